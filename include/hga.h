@@ -1,0 +1,196 @@
+/*
+ * hga.h -- C ABI of libhga.so, the sm_100a Hadamard-GA inner loop.
+ *
+ * The reference (hadamard_ga, pure Python/NumPy) has no FFI of its own; its
+ * "plugin API" is the Python function surface of engine.py:34-55.  Each entry
+ * point below replaces the body of one of those functions (cited per entry),
+ * so a maintainer can bind it from hadamard_ga with ctypes.
+ *
+ * Conventions
+ *   - extern "C", plain pointers and sizes, no torch types.
+ *   - Every pointer named *pop, *cols, *fit, *out, ... is a DEVICE pointer
+ *     (cudaMalloc / torch tensor .data_ptr()).  The library never allocates;
+ *     scratch is passed in after a *_ws_bytes query.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     asynchronous on that stream and never synchronize the host.
+ *   - Return 0 (HGA_OK) or an error code; argument errors are detected on the
+ *     host before any launch.  Data-dependent errors (a point or plan index
+ *     out of range, an entry that is not +-1) are reported through an optional
+ *     device int32 flag the caller reads after synchronizing.
+ *   - Population layouts: "i8" is the reference's int8 (n, m, m) row-major
+ *     array (engine.py:1-21); "packed" is the resident layout of
+ *     paper_2208_14961_b200/csrc/hga_common.cuh: m column records of
+ *     W = ceil(m/32) uint32 words per matrix, bit r%32 of word r/32 set iff
+ *     entry (r, j) is -1.
+ */
+#ifndef HGA_H
+#define HGA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HGA_ABI_VERSION 1
+
+/* return codes */
+#define HGA_OK 0
+#define HGA_E_INVALID 1      /* bad size / shape / enum argument */
+#define HGA_E_UNSUPPORTED 2  /* order or size outside what this build handles */
+#define HGA_E_WORKSPACE 3    /* workspace too small */
+#define HGA_E_CUDA_BASE 1000 /* HGA_E_CUDA_BASE + cudaError_t */
+
+/* penalty variants (bit mask).  F1 = sum|G| - m^2 (core.py:70-78),
+ * F2 = nnz(G) - m (core.py:81-89), ORTH = #{i<j : g_ij = 0},
+ * SQ = sum_{i != j} g_ij^2. */
+#define HGA_VAR_F1 1u
+#define HGA_VAR_F2 2u
+#define HGA_VAR_ORTH 4u
+#define HGA_VAR_SQ 8u
+#define HGA_VAR_ALL 15u
+
+/* device error-flag bits */
+#define HGA_FLAG_NOT_SIGN 1     /* an entry is not +1/-1 */
+#define HGA_FLAG_POINT_RANGE 2  /* crossover point outside [1, m-1] */
+#define HGA_FLAG_PLAN_RANGE 4   /* mutation plan index out of range */
+#define HGA_FLAG_FIT_RANGE 8    /* fitness range exceeds the select histogram */
+
+/* mutation strategies (engine.py:58) */
+#define HGA_MUT_SHARED 0
+#define HGA_MUT_PER_MATRIX 1
+#define HGA_MUT_MULTI 2
+
+int hga_abi_version(void);
+/* pipe-rate microbenchmark: kind 0 = XOR+POPC chains, 1 = LOP3+IADD chains;
+ * each thread runs iters * 8 operations. */
+int hga_probe(int32_t kind, int64_t iters, int32_t blocks, int32_t threads, uint32_t *out,
+              void *stream);
+const char *hga_strerror(int rc);
+int hga_sm_count(int device);
+
+/* ---------------------------------------------------------------- fitness */
+
+/* Replaces engine._fitness_batch / engine.evaluate (engine.py:200-230):
+ * penalties of n int8 (m, m) sign matrices.  Any of f1/f2/orth/sq may be
+ * NULL; `variants` selects which are computed (fused in one pass, the Gram
+ * matrix never leaves the SM).  bad_flag (nullable) gets HGA_FLAG_NOT_SIGN
+ * OR-ed in when an entry is not +-1.  ws is needed only for m > 128
+ * (hga_fitness_i8_ws_bytes). */
+size_t hga_fitness_i8_ws_bytes(int64_t n, int32_t m);
+int hga_fitness_i8(const int8_t *pop, int64_t n, int32_t m, uint32_t variants, int64_t *f1,
+                   int64_t *f2, int64_t *orth, int64_t *sq, int32_t *bad_flag, void *ws,
+                   size_t ws_bytes, void *stream);
+
+/* Same penalties over the packed layout. */
+int hga_fitness_packed(const uint32_t *cols, int64_t n, int32_t m, uint32_t variants,
+                       int64_t *f1, int64_t *f2, int64_t *orth, int64_t *sq, void *stream);
+
+/* int8 (n, m, m) <-> packed conversion (layout edge of the API). */
+int hga_pack_i8(const int8_t *pop, int64_t n, int32_t m, uint32_t *cols, int32_t *bad_flag,
+                void *stream);
+int hga_unpack_i8(const uint32_t *cols, int64_t n, int32_t m, int8_t *pop, void *stream);
+
+/* ------------------------------------------------ reference counter streams */
+
+/* Raw stream words, rand.stream_words (rand.py:69-77) at counters c0..c0+n-1. */
+int hga_ref_words(uint64_t seed, uint64_t stream_id, uint64_t counter0, int64_t n,
+                  uint64_t *out, void *stream);
+/* RngStream(seed, stream_id, counter0).uniform_array(lo, hi, n) (rand.py:122-129). */
+int hga_ref_uniform(uint64_t seed, uint64_t stream_id, uint64_t counter0, int64_t lo,
+                    int64_t hi, int64_t n, int64_t *out, void *stream);
+/* RngStream(seed, stream_id, counter0).permutation(n) (rand.py:131-140),
+ * bit-identical Fisher-Yates. */
+size_t hga_ref_permutation_ws_bytes(int64_t n);
+int hga_ref_permutation(uint64_t seed, uint64_t stream_id, uint64_t counter0, int64_t n,
+                        int64_t *out, void *ws, size_t ws_bytes, void *stream);
+/* engine._random_balanced (engine.py:154-182) into the packed / int8 layout. */
+int hga_ref_init_packed(uint64_t seed, uint64_t purpose, uint64_t generation,
+                        int64_t first_slot, int64_t count, int32_t m, uint32_t *cols,
+                        void *stream);
+int hga_ref_init_i8(uint64_t seed, uint64_t purpose, uint64_t generation, int64_t first_slot,
+                    int64_t count, int32_t m, int8_t *pop, void *stream);
+
+/* ------------------------------------------------------ operators (int8) */
+
+/* engine.crossover (engine.py:257-277) in place on (4N, m, m) int8. */
+int hga_crossover_i8(int8_t *pop, int64_t total, int32_t m, const int64_t *points,
+                     int32_t *bad_flag, void *stream);
+/* engine.mutate (engine.py:339-373) in place on the offspring half. cols is
+ * (total/2, nc), ra/rb are (total/2, nr). */
+int hga_mutate_i8(int8_t *pop, int64_t total, int32_t m, const int64_t *cols,
+                  const int64_t *ra, const int64_t *rb, int32_t nc, int32_t nr,
+                  int32_t *bad_flag, void *stream);
+
+/* select (engine.py:233-248) building blocks.
+ * hga_select_order: order[0:total/2] = argsort(fitness, stable)[:total/2].
+ * Fitness values may be any int64 whose range (max - min) is below
+ * hga_select_max_range(); otherwise HGA_FLAG_FIT_RANGE is raised. */
+int64_t hga_select_max_range(void);
+size_t hga_select_ws_bytes(int64_t total);
+int hga_select_order(const int64_t *fitness, int64_t total, int64_t *order, int32_t *bad_flag,
+                     void *ws, size_t ws_bytes, void *stream);
+/* chosen[s] = order[perm[s]] (s < count); then gathers rows
+ * dst[s] = src[chosen[s]] (layout bytes per matrix given) and
+ * fit_dst[s] = fit_src[chosen[s]] (either may be NULL). */
+int hga_compose_gather(const int64_t *order, const int64_t *perm, int64_t count,
+                       const void *src, void *dst, int64_t bytes_per_matrix,
+                       const int64_t *fit_src, int64_t *fit_dst, int64_t *chosen,
+                       void *stream);
+
+/* -------------------------------------------------- generation (packed) */
+
+/* One generation's crossover + mutation + fitness with EXPLICIT plans
+ * (reference-stream mode; engine.py:449-469 minus select).  Reads the 2N
+ * parents new_pop[0:2N) (already gathered), writes offspring
+ * new_pop[2N:4N) and new_fit[2N:4N) (fitness variant `fit_var`, one bit).
+ * points (N,), cols (2N, nc), ra/rb (2N, nr).  best_key (nullable) gets
+ * atomicMin((fit << 32) | index) over the offspring. */
+int hga_generation_explicit(uint32_t *pop, int64_t *fit, int64_t n_pairs, int32_t m,
+                            const int64_t *points, const int64_t *cols, const int64_t *ra,
+                            const int64_t *rb, int32_t nc, int32_t nr, uint32_t fit_var,
+                            unsigned long long *best_key, void *stream);
+
+/* min over fit[0:n) as (value << 32) | first index, lowest index on ties
+ * (numpy argmin, engine.py:417, 432).  Values must lie in [0, 2^31). */
+int hga_argmin_key(const int64_t *fit, int64_t n, unsigned long long *key, int init,
+                   void *stream);
+
+/* ------------------------------------------------ production GA (Philox) */
+
+/* Arguments of the persistent, grid-synchronised generation loop. */
+typedef struct hga_run_args {
+    /* population ping-pong buffers (packed, 4N matrices each) and fitness */
+    uint32_t *pop[2];
+    int64_t *fit[2];
+    int64_t n_pairs;          /* N */
+    int32_t m;                /* order */
+    int32_t nc, nr;           /* NC, NR */
+    int32_t strategy;         /* HGA_MUT_* */
+    uint32_t fit_var;         /* one of HGA_VAR_F1 / F2 / SQ */
+    int32_t stall_window;     /* 0 = off */
+    uint64_t seed;
+    int64_t max_generation;   /* stop after this absolute generation */
+    int64_t gens_this_call;   /* run at most this many generations now */
+    /* device state (int64[8]): [0] iteration, [1] best fitness,
+     * [2] last restart, [3] current buffer parity, [4] best index,
+     * [5] stop flag, [6..7] reserved */
+    int64_t *state;
+    int64_t *trace;           /* trace[g] = min fitness after generation g */
+    int64_t trace_capacity;
+    uint32_t *best_matrix;    /* packed best-so-far (m * W words) */
+    void *ws;                 /* hga_run_ws_bytes() */
+    size_t ws_bytes;
+} hga_run_args;
+
+size_t hga_run_ws_bytes(int64_t n_pairs, int32_t m);
+/* Philox-stream init of all 4N slots of pop[0] + evaluation + state init. */
+int hga_run_init(const hga_run_args *args, void *stream);
+int hga_run(const hga_run_args *args, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HGA_H */

@@ -1,0 +1,749 @@
+// generation.cu -- one GA generation on the packed resident population.
+//
+//  * hga_generation_explicit: crossover + mutation + fitness with explicit
+//    plans (the reference-stream replay path; select is done beforehand by
+//    hga_select_order + hga_ref_permutation + hga_compose_gather).
+//  * hga_run / hga_run_init: the production loop (engine.py:449-538 with
+//    Philox streams): ONE persistent cooperative kernel runs many
+//    generations; phases are separated by a grid barrier, and the host only
+//    polls an 8-word state block.  Per generation:
+//      A  radix-select histogram of the 4N fitness values (coarse, 4096 bins)
+//      B  threshold tau + tie quota (2N lowest, lowest index first on ties;
+//         engine.py:245), fine histogram if the coarse bin is not exact,
+//         per-CTA counts of (F < tau, F == tau) over contiguous index ranges
+//      D  stable winner ranks by CTA prefix + block scan; rank -> parent slot
+//         through a keyed Feistel bijection (uniformly random placement,
+//         engine.py:246); src[slot] = winner, F_new[slot] = F[winner]
+//      E  fused offspring tiles (generation.cuh) from src[], with the
+//         parents copied to the new buffer (out-of-place gather, engine.py:247)
+//      F  trace / best / stop / stall-restart bookkeeping, replicated in every
+//         CTA from the same global values so all CTAs agree without a barrier
+#include "generation.cuh"
+
+namespace hga {
+
+// ======================================================== explicit plans
+template <int W, int VM>
+__global__ void __launch_bounds__(kGenThreads)
+    k_generation_explicit(uint32_t* pop, int64_t* fit, int64_t N, int m, int ppb,
+                          const int64_t* __restrict__ points, const int64_t* __restrict__ cols,
+                          const int64_t* __restrict__ ra, const int64_t* __restrict__ rb, int nc, int nr,
+                          uint32_t fit_var, unsigned long long* best_key) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const TileSmem s = carve_tile(smem, m, W, ppb, nc, nr);
+    const int64_t mw = (int64_t)m * W;
+    for (int64_t p0 = (int64_t)blockIdx.x * ppb; p0 < N; p0 += (int64_t)gridDim.x * ppb) {
+        const int cnt = (int)min((int64_t)ppb, N - p0);
+        for (int t = threadIdx.x; t < ppb; t += blockDim.x) {
+            if (t < cnt) {
+                s.point[t] = (int16_t)points[p0 + t];
+                s.poff[2 * t] = (p0 + t) * mw;
+                s.poff[2 * t + 1] = (N + p0 + t) * mw;
+            }
+        }
+        for (int t = threadIdx.x; t < 2 * ppb * (nc + 2 * nr); t += blockDim.x) {
+            const int ol = t / (nc + 2 * nr), e = t - ol * (nc + 2 * nr);
+            const int q = ol % ppb;
+            if (q >= cnt) continue;
+            const int64_t row = (ol < ppb) ? p0 + q : N + p0 + q;
+            if (e < nc) s.pcol[ol * nc + e] = (int16_t)cols[row * nc + e];
+            else if (e < nc + nr) s.pra[ol * nr + e - nc] = (int16_t)ra[row * nr + e - nc];
+            else s.prb[ol * nr + e - nc - nr] = (int16_t)rb[row * nr + e - nc - nr];
+        }
+        __syncthreads();
+        offspring_tile<W, VM, false>(s, pop, pop, fit, N, p0, cnt, ppb, m, nc, nr, fit_var, best_key);
+    }
+}
+
+// ======================================================== Philox helpers
+__device__ __forceinline__ U4 draw4(uint64_t seed, uint32_t a, uint32_t b, uint64_t gen, uint32_t purpose) {
+    return philox(U4{a, b, (uint32_t)gen, (purpose << 24) ^ (uint32_t)(gen >> 32)}, (uint32_t)seed,
+                  (uint32_t)(seed >> 32));
+}
+__device__ __forceinline__ uint32_t pick(const U4& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7FEB352Du;
+    x ^= x >> 15;
+    x *= 0x846CA68Bu;
+    x ^= x >> 16;
+    return x;
+}
+
+// Keyed bijection on [0, n) (4-round balanced Feistel + cycle walking).
+__device__ __forceinline__ uint32_t feistel(uint32_t x, uint32_t n, int hb, const U4& k) {
+    const uint32_t mask = (1u << hb) - 1u;
+    do {
+        uint32_t L = x >> hb, R = x & mask;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t f = hash32(R ^ pick(k, r)) & mask;
+            const uint32_t nl = R;
+            R = L ^ f;
+            L = nl;
+        }
+        x = (L << hb) | R;
+    } while (x >= n);
+    return x;
+}
+
+// Philox balanced column (Fisher-Yates over the m rows with Lemire draws).
+template <int W>
+__device__ __forceinline__ void philox_column(uint64_t seed, uint32_t purpose, uint64_t gen, int64_t slot,
+                                              int m, int c, Col<W>& col) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) col.w[w] = 0;
+    if (c == 0) return;
+    const int h = m / 2;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const int lo = 32 * w, hi = min(32 * w + 32, h);
+        if (hi > lo) col.w[w] = (hi - lo == 32) ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u);
+    }
+    U4 r{0, 0, 0, 0};
+    for (int a = 0; a + 1 < m; ++a) {
+        if ((a & 3) == 0)
+            r = draw4(seed, (uint32_t)slot, (uint32_t)c | ((uint32_t)(a >> 2) << 12) | ((uint32_t)(slot >> 32) << 24), gen, purpose);
+        const int b = a + (int)bounded(pick(r, a & 3), (uint32_t)(m - a));
+        swap_rows<W>(col, a, b);
+    }
+}
+
+// ======================================================== grid barrier
+struct Barrier {
+    unsigned int count;
+    unsigned int gen;
+};
+
+__device__ __forceinline__ void grid_sync(Barrier* b) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* vg = &b->gen;
+        const unsigned int g = *vg;
+        __threadfence();
+        if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
+            b->count = 0;
+            __threadfence();
+            atomicExch(&b->gen, g + 1);
+        } else {
+            while (*vg == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ======================================================== run workspace
+constexpr int kHistBins = 4096;
+constexpr int kMaxGrid = 4096;
+
+struct RunWs {
+    Barrier bar;
+    unsigned long long best_key[2];   // per generation parity: min over new population
+    unsigned long long par_key[2];    // min over the parents only (restart bookkeeping)
+    unsigned long long restart_key;
+    uint32_t hist1[kHistBins];
+    uint32_t hist2[kHistBins];
+    uint32_t cnt_lt[kMaxGrid];
+    uint32_t cnt_eq[kMaxGrid];
+    // followed by src[2N] (int64)
+};
+
+__host__ __device__ inline size_t run_ws_head() { return (sizeof(RunWs) + 255) & ~(size_t)255; }
+
+// Block-wide: find the first bin b where the inclusive prefix of h reaches
+// k (1 <= k <= total).  Returns b and the count strictly below b.
+__device__ void find_kth_bin(const uint32_t* h, int bins, uint64_t k, int* out_bin, uint64_t* out_below,
+                             uint64_t* scratch /* >= blockDim/32 + 2 */) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int per = (bins + nt - 1) / nt;
+    const int b0 = tid * per;
+    uint64_t mine = 0;
+    for (int b = b0; b < min(bins, b0 + per); ++b) mine += h[b];
+    // exclusive scan of `mine`
+    uint64_t x = mine;
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) scratch[wid] = x;
+    __syncthreads();
+    if (tid == 0) {
+        uint64_t run = 0;
+        for (int w = 0; w < (nt + 31) / 32; ++w) {
+            const uint64_t t = scratch[w];
+            scratch[w] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+    const uint64_t excl = scratch[wid] + x - mine;
+    __syncthreads();
+    if (excl < k && excl + mine >= k) {
+        uint64_t run = excl;
+        for (int b = b0; b < min(bins, b0 + per); ++b) {
+            if (run + h[b] >= k) {
+                *out_bin = b;
+                *out_below = run;
+                break;
+            }
+            run += h[b];
+        }
+    }
+    __syncthreads();
+}
+
+struct RunParams {
+    hga_run_args a;
+    int W;
+    int ppb;
+    int shift;       // coarse histogram shift
+    int hb;          // Feistel half bits
+};
+
+template <int W, int VM>
+__global__ void __launch_bounds__(kGenThreads) k_run(RunParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t shist[kHistBins];
+    __shared__ uint64_t sscr[40];
+    __shared__ int s_bin;
+    __shared__ uint64_t s_below;
+
+    const hga_run_args& A = P.a;
+    RunWs* ws = reinterpret_cast<RunWs*>(A.ws);
+    int64_t* src = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(A.ws) + run_ws_head());
+    const int64_t N = A.n_pairs, half = 2 * N, total = 4 * N;
+    const int m = A.m;
+    const int64_t mw = (int64_t)m * W;
+    const int nb = gridDim.x, bid = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    const int64_t chunk = (total + nb - 1) / nb;
+    const int64_t lo = min(total, (int64_t)bid * chunk), hi = min(total, lo + chunk);
+    const int nc = A.strategy == HGA_MUT_MULTI ? A.nc : 1;
+    const int nr = A.strategy == HGA_MUT_MULTI ? A.nr : 1;
+    const TileSmem ts = carve_tile(smem, m, W, P.ppb, nc, nr);
+
+    // replicated bookkeeping state (identical in every CTA)
+    int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
+    int parity = (int)A.state[3];
+    int64_t run = A.state[6], last_val = A.state[7];
+    bool stop = A.state[5] != 0;
+
+    for (int64_t gi = 0; gi < A.gens_this_call && !stop; ++gi) {
+        const int64_t gen = iter + 1;
+        const int gp = (int)(gen & 1);
+        const uint32_t* pop_old = A.pop[parity];
+        uint32_t* pop_new = A.pop[parity ^ 1];
+        const int64_t* f_old = A.fit[parity];
+        int64_t* f_new = A.fit[parity ^ 1];
+
+        // ---- A: coarse histogram
+        for (int b = tid; b < kHistBins; b += nt) shist[b] = 0;
+        __syncthreads();
+        for (int64_t i = lo + tid; i < hi; i += nt) atomicAdd(&shist[min((int64_t)kHistBins - 1, f_old[i] >> P.shift)], 1u);
+        __syncthreads();
+        for (int b = tid; b < kHistBins; b += nt)
+            if (shist[b]) atomicAdd(&ws->hist1[b], shist[b]);
+        grid_sync(&ws->bar);
+
+        // ---- B: threshold, tie quota, per-CTA counts
+        find_kth_bin(ws->hist1, kHistBins, (uint64_t)half, &s_bin, &s_below, sscr);
+        int64_t tau;
+        uint64_t quota;
+        if (P.shift == 0) {
+            tau = s_bin;
+            quota = (uint64_t)half - s_below;
+        } else {
+            const int64_t bucket = s_bin;
+            const uint64_t below = s_below;
+            for (int b = tid; b < kHistBins; b += nt) shist[b] = 0;
+            __syncthreads();
+            const int64_t fmask = (1ll << P.shift) - 1;
+            for (int64_t i = lo + tid; i < hi; i += nt) {
+                const int64_t f = f_old[i];
+                if ((f >> P.shift) == bucket) atomicAdd(&shist[f & fmask], 1u);
+            }
+            __syncthreads();
+            for (int b = tid; b < kHistBins; b += nt)
+                if (shist[b]) atomicAdd(&ws->hist2[b], shist[b]);
+            grid_sync(&ws->bar);
+            find_kth_bin(ws->hist2, kHistBins, (uint64_t)half - below, &s_bin, &s_below, sscr);
+            tau = (bucket << P.shift) | s_bin;
+            quota = (uint64_t)half - below - s_below;
+        }
+        {
+            uint32_t nlt = 0, neq = 0;
+            for (int64_t i = lo + tid; i < hi; i += nt) {
+                const int64_t f = f_old[i];
+                nlt += f < tau;
+                neq += f == tau;
+            }
+            nlt = __reduce_add_sync(0xffffffffu, nlt);
+            neq = __reduce_add_sync(0xffffffffu, neq);
+            if ((tid & 31) == 0) {
+                sscr[tid >> 5] = ((uint64_t)nlt << 32) | neq;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                uint64_t a = 0, e = 0;
+                for (int w = 0; w < nt / 32; ++w) {
+                    a += sscr[w] >> 32;
+                    e += sscr[w] & 0xffffffffu;
+                }
+                ws->cnt_lt[bid] = (uint32_t)a;
+                ws->cnt_eq[bid] = (uint32_t)e;
+            }
+        }
+        grid_sync(&ws->bar);
+
+        // ---- D: stable ranks -> Feistel slots
+        {
+            uint64_t lt_b = 0, eq_b = 0;
+            for (int b = tid; b < bid; b += nt) {
+                lt_b += ws->cnt_lt[b];
+                eq_b += ws->cnt_eq[b];
+            }
+            for (int o = 16; o; o >>= 1) {
+                lt_b += __shfl_xor_sync(0xffffffffu, lt_b, o);
+                eq_b += __shfl_xor_sync(0xffffffffu, eq_b, o);
+            }
+            __syncthreads();
+            if ((tid & 31) == 0) sscr[tid >> 5] = (lt_b << 32) | eq_b;
+            __syncthreads();
+            uint64_t lt_run = 0, eq_run = 0;
+            for (int w = 0; w < nt / 32; ++w) {
+                lt_run += sscr[w] >> 32;
+                eq_run += sscr[w] & 0xffffffffu;
+            }
+            __syncthreads();
+            const U4 fk = draw4(A.seed, 0, 0, (uint64_t)gen, (uint32_t)kPSelect);
+            const int lane = tid & 31, wid = tid >> 5;
+            unsigned long long kbest = ~0ull;
+            for (int64_t i0 = lo; i0 < hi; i0 += nt) {
+                const int64_t i = i0 + tid;
+                int64_t f = 0;
+                uint32_t is_lt = 0, is_eq = 0;
+                if (i < hi) {
+                    f = f_old[i];
+                    is_lt = f < tau;
+                    is_eq = f == tau;
+                }
+                // block exclusive scan of (is_lt, is_eq) packed in 16 | 16 bits
+                const uint32_t v = (is_lt << 16) | is_eq;
+                uint32_t x = v;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (lane == 31) sscr[wid] = x;
+                __syncthreads();
+                uint32_t wbase = 0, tot = 0;
+                for (int w = 0; w < nt / 32; ++w) {
+                    const uint32_t t = (uint32_t)sscr[w];
+                    if (w < wid) wbase += t;
+                    tot += t;
+                }
+                const uint32_t excl = wbase + x - v;
+                const uint64_t lt_rank = lt_run + (excl >> 16);
+                const uint64_t eq_rank = eq_run + (excl & 0xffffu);
+                if (is_lt || (is_eq && eq_rank < quota)) {
+                    const uint64_t rank = lt_rank + min(eq_rank, quota);
+                    const uint32_t slot = feistel((uint32_t)rank, (uint32_t)half, P.hb, fk);
+                    src[slot] = i;
+                    f_new[slot] = f;
+                    kbest = min(kbest, ((unsigned long long)f << 32) | slot);
+                }
+                lt_run += tot >> 16;
+                eq_run += tot & 0xffffu;
+                __syncthreads();
+            }
+            for (int o = 16; o; o >>= 1) kbest = min(kbest, __shfl_xor_sync(0xffffffffu, kbest, o));
+            if (lane == 0 && kbest != ~0ull) {
+                atomicMin(&ws->best_key[gp], kbest);
+                atomicMin(&ws->par_key[gp], kbest);
+            }
+        }
+        grid_sync(&ws->bar);
+
+        // ---- E: offspring tiles
+        if (bid == 0) {
+            for (int b = tid; b < kHistBins; b += nt) {
+                ws->hist1[b] = 0;
+                ws->hist2[b] = 0;
+            }
+        }
+        {
+            const int ppb = P.ppb;
+            const int per_off = nc + 2 * nr;
+            const int blocks4 = (per_off + 3) / 4;
+            for (int64_t p0 = (int64_t)bid * ppb; p0 < N; p0 += (int64_t)nb * ppb) {
+                const int cnt = (int)min((int64_t)ppb, N - p0);
+                if (tid < cnt) {
+                    const int64_t p = p0 + tid;
+                    const U4 r = draw4(A.seed, (uint32_t)p, (uint32_t)(p >> 32), (uint64_t)gen, (uint32_t)kPCrossover);
+                    ts.point[tid] = (int16_t)(1 + bounded(r.x, (uint32_t)(m - 1)));
+                    ts.poff[2 * tid] = src[p] * mw;
+                    ts.poff[2 * tid + 1] = src[N + p] * mw;
+                }
+                for (int t = tid; t < 2 * ppb * blocks4; t += nt) {
+                    const int ol = t / blocks4, blk = t - ol * blocks4;
+                    const int q = ol % ppb;
+                    if (q >= cnt) continue;
+                    int64_t o = (ol < ppb) ? p0 + q : N + p0 + q;  // plan row, as engine.py
+                    if (A.strategy == HGA_MUT_SHARED) o = 0;
+                    const U4 r = draw4(A.seed, (uint32_t)o, (uint32_t)blk | ((uint32_t)(o >> 32) << 16), (uint64_t)gen,
+                                       (uint32_t)kPMutCol);
+#pragma unroll
+                    for (int e4 = 0; e4 < 4; ++e4) {
+                        const int e = blk * 4 + e4;
+                        const uint32_t rv = pick(r, e4);
+                        if (e < nc) ts.pcol[ol * nc + e] = (int16_t)(1 + bounded(rv, (uint32_t)(m - 1)));
+                        else if (e < nc + nr) ts.pra[ol * nr + e - nc] = (int16_t)bounded(rv, (uint32_t)m);
+                        else if (e < per_off) ts.prb[ol * nr + e - nc - nr] = (int16_t)bounded(rv, (uint32_t)m);
+                    }
+                }
+                __syncthreads();
+                offspring_tile<W, VM, true>(ts, pop_old, pop_new, f_new, N, p0, cnt, ppb, m, nc, nr, A.fit_var,
+                                            &ws->best_key[gp]);
+            }
+        }
+        grid_sync(&ws->bar);
+
+        // ---- F: bookkeeping (every CTA computes the same decisions)
+        {
+            const unsigned long long key = *(volatile unsigned long long*)&ws->best_key[gp];
+            const int64_t v = (int64_t)(key >> 32);
+            const int64_t idx = (int64_t)(key & 0xffffffffu);
+            iter = gen;
+            parity ^= 1;
+            run = (v == last_val) ? run + 1 : 1;
+            last_val = v;
+            const bool improved = v < best;
+            if (improved) best = v;
+            if (bid == 0) {
+                if (gen < A.trace_capacity) A.trace[gen] = v;
+                if (improved) {
+                    for (int64_t t = tid; t < mw; t += nt) A.best_matrix[t] = pop_new[idx * mw + t];
+                    if (tid == 0) A.state[4] = idx;
+                }
+                if (tid == 0) {
+                    ws->best_key[gp ^ 1] = ~0ull;
+                    ws->par_key[gp ^ 1] = ~0ull;
+                }
+            }
+            stop = best == 0 || iter >= A.max_generation;
+            // stall restart (engine.py:472-494, 518-525)
+            if (!stop && A.stall_window > 0 && iter - last_restart >= A.stall_window && run >= A.stall_window &&
+                last_val > 0) {
+                // refill offspring slots of the new population, evaluate them
+                uint32_t* cur = pop_new;
+                int64_t* fcur = f_new;
+                const int64_t work = half * m;
+                for (int64_t t0 = (int64_t)bid * nt; t0 < work; t0 += (int64_t)nb * nt) {
+                    const int64_t t = t0 + tid;
+                    if (t < work) {
+                        const int64_t s = half + t / m;
+                        const int c = (int)(t % m);
+                        Col<W> col;
+                        philox_column<W>(A.seed, (uint32_t)kPRestart, (uint64_t)iter, s, m, c, col);
+#pragma unroll
+                        for (int w = 0; w < W; ++w) cur[s * mw + (int64_t)c * W + w] = col.w[w];
+                    }
+                }
+                grid_sync(&ws->bar);
+                // evaluate fresh offspring with the fitness tile (pairs of slots)
+                {
+                    const int mpb = 2 * P.ppb;  // matches the tile's shared-memory carve
+                    const int kl = tid / m, i = tid - kl * m;
+                    const int hlf = (m & 1) ? -1 : m / 2;
+                    for (int64_t k0 = half + (int64_t)bid * mpb; k0 < total; k0 += (int64_t)nb * mpb) {
+                        const int cnt = (int)min((int64_t)mpb, total - k0);
+                        const bool act = kl < cnt && kl < mpb;
+                        Col<W> c;
+                        if (act) {
+#pragma unroll
+                            for (int w = 0; w < W; ++w) c.w[w] = cur[(k0 + kl) * mw + (int64_t)i * W + w];
+                            uint32_t* d = ts.col + ((int64_t)kl * 2 * m + i) * W;
+#pragma unroll
+                            for (int w = 0; w < W; ++w) {
+                                d[w] = c.w[w];
+                                d[(int64_t)m * W + w] = c.w[w];
+                            }
+                        }
+                        if (tid < mpb * 3) ts.acc[tid] = 0;
+                        __syncthreads();
+                        Acc a{0, 0, 0};
+                        if (act) {
+                            const uint32_t* base = ts.col + ((int64_t)kl * 2 * m + i) * W;
+                            const int steps = pair_steps(m, i);
+                            for (int d = 1; d <= steps; ++d) {
+                                int p = 0;
+#pragma unroll
+                                for (int w = 0; w < W; ++w) p += __popc(c.w[w] ^ base[d * W + w]);
+                                acc_pair<VM>(a, p, m, hlf);
+                            }
+                        }
+                        if (act) {
+                            if (VM & HGA_VAR_F1) atomicAdd(&ts.acc[kl * 3 + 0], a.s1);
+                            if (VM & HGA_VAR_F2) atomicAdd(&ts.acc[kl * 3 + 1], a.s2);
+                            if (VM & HGA_VAR_SQ) atomicAdd(&ts.acc[kl * 3 + 2], a.s4);
+                        }
+                        __syncthreads();
+                        if (tid < cnt) {
+                            const uint32_t* ac = ts.acc + tid * 3;
+                            const int64_t fv = 2 * (int64_t)(A.fit_var == HGA_VAR_F1 ? ac[0] : A.fit_var == HGA_VAR_SQ ? ac[2] : ac[1]);
+                            fcur[k0 + tid] = fv;
+                            atomicMin(&ws->restart_key, ((unsigned long long)fv << 32) | (unsigned long long)(k0 + tid));
+                        }
+                        __syncthreads();
+                    }
+                }
+                grid_sync(&ws->bar);
+                const unsigned long long rk = *(volatile unsigned long long*)&ws->restart_key;
+                const unsigned long long pk = *(volatile unsigned long long*)&ws->par_key[gp];
+                const unsigned long long k2 = min(rk, pk);
+                const int64_t v2 = (int64_t)(k2 >> 32);
+                if (v2 < best) {
+                    best = v2;
+                    if (bid == 0) {
+                        const int64_t id2 = (int64_t)(k2 & 0xffffffffu);
+                        for (int64_t t = tid; t < mw; t += nt) A.best_matrix[t] = cur[id2 * mw + t];
+                        if (tid == 0) A.state[4] = id2;
+                    }
+                }
+                last_restart = iter;
+                grid_sync(&ws->bar);
+                if (bid == 0 && tid == 0) ws->restart_key = ~0ull;
+                stop = best == 0;
+            }
+        }
+    }
+    if (bid == 0 && tid == 0) {
+        A.state[0] = iter;
+        A.state[1] = best;
+        A.state[2] = last_restart;
+        A.state[3] = parity;
+        A.state[5] = stop ? 1 : 0;
+        A.state[6] = run;
+        A.state[7] = last_val;
+    }
+}
+
+// ======================================================== run init
+template <int W>
+__global__ void k_philox_init(uint64_t seed, uint32_t purpose, uint64_t gen, int64_t first_slot, int64_t count, int m,
+                              uint32_t* __restrict__ cols) {
+    const int64_t total = count * m;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = first_slot + t / m;
+        const int c = (int)(t % m);
+        Col<W> col;
+        philox_column<W>(seed, purpose, gen, s, m, c, col);
+#pragma unroll
+        for (int w = 0; w < W; ++w) cols[(s * m + c) * W + w] = col.w[w];
+    }
+}
+
+__global__ void k_run_finish_init(hga_run_args a, int W, unsigned long long* key, RunWs* ws) {
+    const unsigned long long k = *key;
+    const int64_t v = (int64_t)(k >> 32), idx = (int64_t)(k & 0xffffffffu);
+    const int64_t mw = (int64_t)a.m * W;
+    for (int64_t t = threadIdx.x; t < mw; t += blockDim.x) a.best_matrix[t] = a.pop[0][idx * mw + t];
+    if (threadIdx.x == 0) {
+        a.state[0] = 0;
+        a.state[1] = v;
+        a.state[2] = 0;
+        a.state[3] = 0;
+        a.state[4] = idx;
+        a.state[5] = v == 0 ? 1 : 0;
+        a.state[6] = 1;
+        a.state[7] = v;
+        if (a.trace_capacity > 0) a.trace[0] = v;
+        ws->bar.count = 0;
+        ws->bar.gen = 0;
+        ws->best_key[0] = ws->best_key[1] = ~0ull;
+        ws->par_key[0] = ws->par_key[1] = ~0ull;
+        ws->restart_key = ~0ull;
+    }
+    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
+        ws->hist1[b] = 0;
+        ws->hist2[b] = 0;
+    }
+}
+
+__global__ void k_argmin_key2(const int64_t* __restrict__ f, int64_t n, unsigned long long* key) {
+    unsigned long long best = ~0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        best = min(best, ((unsigned long long)f[i] << 32) | (unsigned long long)i);
+    for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) atomicMin(key, best);
+}
+
+static int bit_length(uint64_t x) {
+    int b = 0;
+    while (x) {
+        ++b;
+        x >>= 1;
+    }
+    return b;
+}
+
+static uint64_t max_fitness(int m, uint32_t v) {
+    const uint64_t M = (uint64_t)m;
+    if (v == HGA_VAR_F1) return M * M * (M - 1);
+    if (v == HGA_VAR_SQ) return M * M * M * (M - 1);
+    return M * (M - 1);
+}
+
+template <int W, int VM>
+static int launch_run(const hga_run_args* a, cudaStream_t st) {
+    RunParams P;
+    P.a = *a;
+    P.W = W;
+    const int nc = a->strategy == HGA_MUT_MULTI ? a->nc : 1;
+    const int nr = a->strategy == HGA_MUT_MULTI ? a->nr : 1;
+    P.ppb = kGenThreads / (2 * a->m);
+    const int bits = bit_length(max_fitness(a->m, a->fit_var));
+    P.shift = bits > 12 ? bits - 12 : 0;
+    const int dom_bits = std::max(2, bit_length((uint64_t)(2 * a->n_pairs - 1)));
+    P.hb = (dom_bits + 1) / 2;
+    const size_t smem = tile_smem_bytes(a->m, W, P.ppb, nc, nr);
+    auto kern = k_run<W, VM>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return to_rc(e);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGenThreads, smem);
+    if (e != cudaSuccess) return to_rc(e);
+    if (per_sm < 1) return HGA_E_UNSUPPORTED;
+    int grid = sm_count_cached() * std::min(per_sm, 2);
+    grid = std::min(grid, kMaxGrid);
+    const int64_t want = std::max<int64_t>(1, (a->n_pairs + P.ppb - 1) / P.ppb);
+    grid = (int)std::min<int64_t>(grid, std::max<int64_t>(want, 1));
+    void* params[] = {&P};
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kGenThreads), params, smem, st);
+    return to_rc(e);
+}
+
+template <int W>
+static int launch_run_w(const hga_run_args* a, cudaStream_t st) {
+    switch (a->fit_var) {
+        case HGA_VAR_F1: return launch_run<W, HGA_VAR_F1>(a, st);
+        case HGA_VAR_SQ: return launch_run<W, HGA_VAR_SQ>(a, st);
+        default: return launch_run<W, HGA_VAR_F2>(a, st);
+    }
+}
+
+template <int W, int VM>
+static int launch_explicit(uint32_t* pop, int64_t* fit, int64_t N, int m, const int64_t* points, const int64_t* cols,
+                           const int64_t* ra, const int64_t* rb, int nc, int nr, uint32_t fit_var,
+                           unsigned long long* best_key, cudaStream_t st) {
+    const int ppb = kGenThreads / (2 * m);
+    const size_t smem = tile_smem_bytes(m, W, ppb, nc, nr);
+    auto kern = k_generation_explicit<W, VM>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return to_rc(e);
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGenThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t tiles = (N + ppb - 1) / ppb;
+    const int64_t grid = std::min<int64_t>(tiles, (int64_t)sm_count_cached() * per_sm);
+    kern<<<(unsigned)grid, kGenThreads, smem, st>>>(pop, fit, N, m, ppb, points, cols, ra, rb, nc, nr, fit_var, best_key);
+    return to_rc(cudaGetLastError());
+}
+
+template <int W>
+static int launch_explicit_w(uint32_t* pop, int64_t* fit, int64_t N, int m, const int64_t* points,
+                             const int64_t* cols, const int64_t* ra, const int64_t* rb, int nc, int nr,
+                             uint32_t fit_var, unsigned long long* best_key, cudaStream_t st) {
+    switch (fit_var) {
+        case HGA_VAR_F1: return launch_explicit<W, HGA_VAR_F1>(pop, fit, N, m, points, cols, ra, rb, nc, nr, fit_var, best_key, st);
+        case HGA_VAR_SQ: return launch_explicit<W, HGA_VAR_SQ>(pop, fit, N, m, points, cols, ra, rb, nc, nr, fit_var, best_key, st);
+        default: return launch_explicit<W, HGA_VAR_F2>(pop, fit, N, m, points, cols, ra, rb, nc, nr, fit_var, best_key, st);
+    }
+}
+
+}  // namespace hga
+
+using namespace hga;
+
+static bool valid_var(uint32_t v) { return v == HGA_VAR_F1 || v == HGA_VAR_F2 || v == HGA_VAR_SQ; }
+
+extern "C" {
+
+int hga_generation_explicit(uint32_t* pop, int64_t* fit, int64_t n_pairs, int32_t m, const int64_t* points,
+                            const int64_t* cols, const int64_t* ra, const int64_t* rb, int32_t nc, int32_t nr,
+                            uint32_t fit_var, unsigned long long* best_key, void* stream) {
+    if (n_pairs < 0 || m < 2 || m > 32 * kMaxRegWords || nc < 1 || nr < 1 || nc > 4096 || nr > 4096 ||
+        !valid_var(fit_var))
+        return HGA_E_INVALID;
+    if (n_pairs == 0) return HGA_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (words_for(m)) {
+        case 1: return launch_explicit_w<1>(pop, fit, n_pairs, m, points, cols, ra, rb, nc, nr, fit_var, best_key, st);
+        case 2: return launch_explicit_w<2>(pop, fit, n_pairs, m, points, cols, ra, rb, nc, nr, fit_var, best_key, st);
+        case 3: return launch_explicit_w<3>(pop, fit, n_pairs, m, points, cols, ra, rb, nc, nr, fit_var, best_key, st);
+        default: return launch_explicit_w<4>(pop, fit, n_pairs, m, points, cols, ra, rb, nc, nr, fit_var, best_key, st);
+    }
+}
+
+size_t hga_run_ws_bytes(int64_t n_pairs, int32_t m) {
+    (void)m;
+    return run_ws_head() + (size_t)(2 * n_pairs) * 8;
+}
+
+static int run_args_ok(const hga_run_args* a) {
+    if (!a || a->n_pairs < 1 || a->m < 4 || a->m > 32 * kMaxRegWords || (a->m & 3) || !valid_var(a->fit_var))
+        return 0;
+    if (a->strategy < 0 || a->strategy > 2 || a->nc < 1 || a->nc > a->m - 1 || a->nr < 1 || a->nr > a->m / 2) return 0;
+    if (4 * a->n_pairs >= ((int64_t)1 << 31)) return 0;  // 32-bit slot ids in the select keys
+    if (bit_length(max_fitness(a->m, a->fit_var)) > 24) return 0;
+    if (!a->pop[0] || !a->pop[1] || !a->fit[0] || !a->fit[1] || !a->state || !a->best_matrix || !a->ws) return 0;
+    if (a->ws_bytes < hga_run_ws_bytes(a->n_pairs, a->m)) return 0;
+    return 1;
+}
+
+int hga_run_init(const hga_run_args* a, void* stream) {
+    if (!run_args_ok(a)) return HGA_E_INVALID;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int m = a->m, W = words_for(m);
+    const int64_t total = 4 * a->n_pairs;
+    const int64_t work = total * m;
+    const int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)sm_count_cached() * 16);
+    switch (W) {
+        case 1: k_philox_init<1><<<grid, 256, 0, st>>>(a->seed, (uint32_t)kPInit, 0, 0, total, m, a->pop[0]); break;
+        case 2: k_philox_init<2><<<grid, 256, 0, st>>>(a->seed, (uint32_t)kPInit, 0, 0, total, m, a->pop[0]); break;
+        case 3: k_philox_init<3><<<grid, 256, 0, st>>>(a->seed, (uint32_t)kPInit, 0, 0, total, m, a->pop[0]); break;
+        default: k_philox_init<4><<<grid, 256, 0, st>>>(a->seed, (uint32_t)kPInit, 0, 0, total, m, a->pop[0]); break;
+    }
+    int rc = hga_fitness_packed(a->pop[0], total, m, a->fit_var, a->fit_var == HGA_VAR_F1 ? a->fit[0] : nullptr,
+                                a->fit_var == HGA_VAR_F2 ? a->fit[0] : nullptr, nullptr,
+                                a->fit_var == HGA_VAR_SQ ? a->fit[0] : nullptr, stream);
+    if (rc) return rc;
+    RunWs* ws = (RunWs*)a->ws;
+    unsigned long long* key = &ws->restart_key;
+    cudaError_t e = cudaMemsetAsync(key, 0xFF, 8, st);
+    if (e != cudaSuccess) return to_rc(e);
+    k_argmin_key2<<<(int)std::min<int64_t>((total + 255) / 256, sm_count_cached() * 8), 256, 0, st>>>(a->fit[0], total, key);
+    k_run_finish_init<<<1, 256, 0, st>>>(*a, W, key, ws);
+    return to_rc(cudaGetLastError());
+}
+
+int hga_run(const hga_run_args* a, void* stream) {
+    if (!run_args_ok(a)) return HGA_E_INVALID;
+    if (a->gens_this_call <= 0) return HGA_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (words_for(a->m)) {
+        case 1: return launch_run_w<1>(a, st);
+        case 2: return launch_run_w<2>(a, st);
+        case 3: return launch_run_w<3>(a, st);
+        default: return launch_run_w<4>(a, st);
+    }
+}
+
+}  // extern "C"

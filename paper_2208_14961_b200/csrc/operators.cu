@@ -1,0 +1,318 @@
+// operators.cu -- the reference's select / crossover / mutate on device
+// (engine.py:233-373), with the reference's exact semantics.
+//
+//   crossover_i8   engine.crossover   (engine.py:257-277), int8 layout, in place
+//   mutate_i8      engine.mutate      (engine.py:339-373), int8 layout, in place
+//   select_order   argsort(F, stable)[:total/2]             (engine.py:245)
+//   compose_gather chosen = order[perm]; rows/fitness gather (engine.py:246-248)
+//   argmin_key     first-minimum argmin                      (engine.py:417, 432)
+#include "hga_common.cuh"
+
+namespace hga {
+
+static int grid_1d(int64_t work, int threads = 256) {
+    int64_t g = (work + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)sm_count_cached() * 16));
+}
+
+// ------------------------------------------------------------- crossover
+// One thread per (pair, row): 4-byte chunks with a byte mask at the split.
+__global__ void k_crossover_i8(int8_t* pop, int64_t n_pairs, int m, const int64_t* __restrict__ points,
+                               int32_t* bad_flag) {
+    const int64_t mm = (int64_t)m * m;
+    const int64_t work = n_pairs * m;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < work;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = t / m;
+        const int r = (int)(t - p * m);
+        const int64_t c = points[p];
+        if (c < 1 || c > m - 1) {
+            if (r == 0 && bad_flag) atomicOr(bad_flag, HGA_FLAG_POINT_RANGE);
+            continue;
+        }
+        const int64_t row = (int64_t)r * m;
+        const int8_t* a = pop + p * mm + row;
+        const int8_t* b = pop + (n_pairs + p) * mm + row;
+        int8_t* o1 = pop + (2 * n_pairs + p) * mm + row;
+        int8_t* o2 = pop + (3 * n_pairs + p) * mm + row;
+        if ((m & 3) == 0 && ((((uintptr_t)pop) & 3) == 0)) {
+            for (int j0 = 0; j0 < m; j0 += 4) {
+                const uint32_t x = *reinterpret_cast<const uint32_t*>(a + j0);
+                const uint32_t y = *reinterpret_cast<const uint32_t*>(b + j0);
+                const int64_t keep = c - j0;  // leading bytes of this chunk taken from the "left" parent
+                const uint32_t mask = keep >= 4 ? 0xFFFFFFFFu : (keep <= 0 ? 0u : ((1u << (8 * keep)) - 1u));
+                *reinterpret_cast<uint32_t*>(o1 + j0) = (x & mask) | (y & ~mask);
+                *reinterpret_cast<uint32_t*>(o2 + j0) = (y & mask) | (x & ~mask);
+            }
+        } else {
+            for (int j = 0; j < m; ++j) {
+                const int8_t x = a[j], y = b[j];
+                o1[j] = j < c ? x : y;
+                o2[j] = j < c ? y : x;
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------- mutate
+// One thread per offspring; columns in plan order, row pairs inner, exactly
+// the reference's sequential semantics (duplicates re-apply).
+__global__ void k_mutate_i8(int8_t* pop, int64_t half, int m, const int64_t* __restrict__ cols,
+                            const int64_t* __restrict__ ra, const int64_t* __restrict__ rb, int nc,
+                            int nr, int32_t* bad_flag) {
+    const int64_t mm = (int64_t)m * m;
+    for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < half;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        bool ok = true;
+        for (int jc = 0; jc < nc; ++jc) ok &= cols[o * nc + jc] >= 1 && cols[o * nc + jc] <= m - 1;
+        for (int ir = 0; ir < nr; ++ir)
+            ok &= ra[o * nr + ir] >= 0 && ra[o * nr + ir] <= m - 1 && rb[o * nr + ir] >= 0 && rb[o * nr + ir] <= m - 1;
+        if (!ok) {
+            if (bad_flag) atomicOr(bad_flag, HGA_FLAG_PLAN_RANGE);
+            continue;
+        }
+        int8_t* q = pop + (half + o) * mm;
+        for (int jc = 0; jc < nc; ++jc) {
+            const int64_t c = cols[o * nc + jc];
+            for (int ir = 0; ir < nr; ++ir) {
+                int8_t* x = q + ra[o * nr + ir] * m + c;
+                int8_t* y = q + rb[o * nr + ir] * m + c;
+                const int8_t u = *x, v = *y;
+                if (u != v) {
+                    *x = v;
+                    *y = u;
+                }
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------- select
+// Stable order of the `half` smallest fitness values: histogram over
+// (F - min), exclusive scan, then one warp scatters indices in index order
+// (match_any groups equal values inside a 32-wide chunk, so equal values keep
+// index order -- the stable-argsort tie rule).
+constexpr int64_t kSelMaxRange = 1 << 22;
+constexpr int64_t kSelSmemBins = 40 * 1024;
+
+struct SelWs {
+    long long mn, mx;
+};
+
+__global__ void k_sel_minmax(const int64_t* __restrict__ f, int64_t n, SelWs* w) {
+    long long mn = LLONG_MAX, mx = LLONG_MIN;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        mn = min(mn, (long long)f[i]);
+        mx = max(mx, (long long)f[i]);
+    }
+    for (int o = 16; o; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&w->mn, mn);
+        atomicMax(&w->mx, mx);
+    }
+}
+
+__global__ void k_sel_init(SelWs* w) {
+    w->mn = LLONG_MAX;
+    w->mx = LLONG_MIN;
+}
+
+__global__ void k_sel_hist(const int64_t* __restrict__ f, int64_t n, const SelWs* w, int32_t* hist,
+                           int32_t* bad_flag) {
+    const long long mn = w->mn;
+    if ((unsigned long long)(w->mx - mn) >= (unsigned long long)kSelMaxRange) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && bad_flag) atomicOr(bad_flag, HGA_FLAG_FIT_RANGE);
+        return;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&hist[f[i] - mn], 1);
+}
+
+// Single CTA: scan hist -> start offsets, then the ordered scatter.
+__global__ void __launch_bounds__(1024) k_sel_scatter(const int64_t* __restrict__ f, int64_t n,
+                                                      int64_t half, const SelWs* w, int32_t* hist,
+                                                      int64_t* order) {
+    extern __shared__ int32_t sbins[];
+    __shared__ int32_t warp_tot[32];
+    __shared__ int32_t carry;
+    const long long mn = w->mn;
+    if ((unsigned long long)(w->mx - mn) >= (unsigned long long)kSelMaxRange) return;
+    const int64_t R = w->mx - mn + 1;
+    const bool in_smem = R <= kSelSmemBins;
+    int32_t* cur = in_smem ? sbins : hist;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    // block-wide exclusive scan over R bins, 1024 at a time
+    for (int64_t b0 = 0; b0 < R; b0 += 1024) {
+        const int64_t b = b0 + tid;
+        const int32_t v = b < R ? hist[b] : 0;
+        int32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int32_t t = warp_tot[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            warp_tot[lane] = t;
+        }
+        __syncthreads();
+        const int32_t excl = carry + (wid ? warp_tot[wid - 1] : 0) + x - v;
+        if (b < R) cur[b] = excl;
+        __syncthreads();
+        if (tid == 0) carry += warp_tot[31];
+        __syncthreads();
+    }
+    // ordered scatter by warp 0
+    if (wid == 0) {
+        for (int64_t i0 = 0; i0 < n; i0 += 32) {
+            const int64_t i = i0 + lane;
+            int64_t key = -1;
+            int32_t start = 0;
+            if (i < n) {
+                key = f[i] - mn;
+                start = cur[key];
+                if (start >= half) key = -1;
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            if (key >= 0) {
+                const int rank = __popc(peers & ((1u << lane) - 1u));
+                const int64_t pos = (int64_t)start + rank;
+                if (pos < half) order[pos] = i;
+            }
+            __syncwarp();
+            if (key >= 0 && (__ffs(peers) - 1) == lane) cur[key] = start + __popc(peers);
+            __syncwarp();
+        }
+    }
+}
+
+// -------------------------------------------------------- compose + gather
+template <typename V>
+__global__ void k_compose_gather(const int64_t* __restrict__ order, const int64_t* __restrict__ perm,
+                                 int64_t count, const V* __restrict__ src, V* __restrict__ dst,
+                                 int64_t vec_per_matrix, const int64_t* __restrict__ fit_src,
+                                 int64_t* __restrict__ fit_dst, int64_t* __restrict__ chosen) {
+    const int64_t work = count * vec_per_matrix;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < work;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t / vec_per_matrix;
+        const int64_t v = t - s * vec_per_matrix;
+        const int64_t c = perm ? order[perm[s]] : order[s];
+        if (src) dst[s * vec_per_matrix + v] = src[c * vec_per_matrix + v];
+        if (v == 0) {
+            if (fit_dst) fit_dst[s] = fit_src[c];
+            if (chosen) chosen[s] = c;
+        }
+    }
+}
+
+// ----------------------------------------------------------------- argmin
+__global__ void k_argmin_key(const int64_t* __restrict__ f, int64_t n, unsigned long long* key) {
+    unsigned long long best = ~0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        best = min(best, ((unsigned long long)f[i] << 32) | (unsigned long long)i);
+    for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) atomicMin(key, best);
+}
+
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
+}  // namespace hga
+
+using namespace hga;
+
+extern "C" {
+
+int hga_crossover_i8(int8_t* pop, int64_t total, int32_t m, const int64_t* points, int32_t* bad_flag,
+                     void* stream) {
+    if (total < 0 || total % 4 || m < 1) return HGA_E_INVALID;
+    if (total == 0 || m == 1) return HGA_OK;
+    const int64_t np_ = total / 4;
+    k_crossover_i8<<<grid_1d(np_ * m), 256, 0, (cudaStream_t)stream>>>(pop, np_, m, points, bad_flag);
+    return to_rc(cudaGetLastError());
+}
+
+int hga_mutate_i8(int8_t* pop, int64_t total, int32_t m, const int64_t* cols, const int64_t* ra,
+                  const int64_t* rb, int32_t nc, int32_t nr, int32_t* bad_flag, void* stream) {
+    if (total < 0 || total % 2 || m < 1 || nc < 0 || nr < 0) return HGA_E_INVALID;
+    const int64_t half = total / 2;
+    if (half == 0 || nc == 0 || nr == 0) return HGA_OK;
+    k_mutate_i8<<<grid_1d(half, 128), 128, 0, (cudaStream_t)stream>>>(pop, half, m, cols, ra, rb, nc, nr, bad_flag);
+    return to_rc(cudaGetLastError());
+}
+
+int64_t hga_select_max_range(void) { return kSelMaxRange; }
+
+size_t hga_select_ws_bytes(int64_t total) {
+    (void)total;
+    return 256 + (size_t)kSelMaxRange * 4;
+}
+
+int hga_select_order(const int64_t* fitness, int64_t total, int64_t* order, int32_t* bad_flag, void* ws,
+                     size_t ws_bytes, void* stream) {
+    if (total < 0) return HGA_E_INVALID;
+    const int64_t half = total / 2;
+    if (half == 0) return HGA_OK;
+    if (!ws || ws_bytes < hga_select_ws_bytes(total)) return HGA_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    SelWs* w = (SelWs*)ws;
+    int32_t* hist = (int32_t*)((char*)ws + 256);
+    cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)kSelMaxRange * 4, st);
+    if (e != cudaSuccess) return to_rc(e);
+    k_sel_init<<<1, 1, 0, st>>>(w);
+    k_sel_minmax<<<grid_1d(total), 256, 0, st>>>(fitness, total, w);
+    k_sel_hist<<<grid_1d(total), 256, 0, st>>>(fitness, total, w, hist, bad_flag);
+    const size_t smem = (size_t)kSelSmemBins * 4;
+    e = cudaFuncSetAttribute(k_sel_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return to_rc(e);
+    k_sel_scatter<<<1, 1024, smem, st>>>(fitness, total, half, w, hist, order);
+    return to_rc(cudaGetLastError());
+}
+
+int hga_compose_gather(const int64_t* order, const int64_t* perm, int64_t count, const void* src, void* dst,
+                       int64_t bytes_per_matrix, const int64_t* fit_src, int64_t* fit_dst, int64_t* chosen,
+                       void* stream) {
+    if (count < 0 || bytes_per_matrix < 0) return HGA_E_INVALID;
+    if (count == 0) return HGA_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const uintptr_t al = (uintptr_t)src | (uintptr_t)dst | (uintptr_t)bytes_per_matrix;
+    if (!src || bytes_per_matrix == 0) {
+        k_compose_gather<uint8_t><<<grid_1d(count), 256, 0, st>>>(order, perm, count, nullptr, nullptr, 1,
+                                                                   fit_src, fit_dst, chosen);
+    } else if ((al & 15) == 0) {
+        const int64_t v = bytes_per_matrix / 16;
+        k_compose_gather<uint4><<<grid_1d(count * v), 256, 0, st>>>(order, perm, count, (const uint4*)src,
+                                                                    (uint4*)dst, v, fit_src, fit_dst, chosen);
+    } else if ((al & 3) == 0) {
+        const int64_t v = bytes_per_matrix / 4;
+        k_compose_gather<uint32_t><<<grid_1d(count * v), 256, 0, st>>>(order, perm, count, (const uint32_t*)src,
+                                                                        (uint32_t*)dst, v, fit_src, fit_dst, chosen);
+    } else {
+        k_compose_gather<uint8_t><<<grid_1d(count * bytes_per_matrix), 256, 0, st>>>(
+            order, perm, count, (const uint8_t*)src, (uint8_t*)dst, bytes_per_matrix, fit_src, fit_dst, chosen);
+    }
+    return to_rc(cudaGetLastError());
+}
+
+int hga_argmin_key(const int64_t* fit, int64_t n, unsigned long long* key, int init, void* stream) {
+    if (n < 0) return HGA_E_INVALID;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (init) k_set_u64<<<1, 1, 0, st>>>(key, ~0ull);
+    if (n > 0) k_argmin_key<<<grid_1d(n), 256, 0, st>>>(fit, n, key);
+    return to_rc(cudaGetLastError());
+}
+
+}  // extern "C"

@@ -1,0 +1,737 @@
+"""GA inner loop on B200 -- drop-in for hadamard_ga.engine (engine.py:1-538).
+
+Same names, argument order, return types and errors as the reference's
+engine module (engine.py:34-55); the work runs in sm_100a kernels through
+libhga (include/hga.h), with torch owning device memory.  No CPU fallback.
+
+Population layouts
+    * API edge: the reference's int8 (4N, m, m) row-major array, as numpy
+      (copied to/from the GPU) or as a CUDA int8 tensor (used in place).
+    * Resident (SearchState): bit-packed columns, m * ceil(m/32) uint32
+      words per matrix (12.5-25x smaller than int8), ping-pong buffers.
+
+Random streams (GAConfig.rng)
+    * "reference": the reference's splitmix64 counter streams, reproduced on
+      device bit-for-bit; a seeded run returns the identical RunRecord
+      (trace, iterations, best matrix) as hadamard_ga.run_search.  Population
+      limits are the reference's (its stream-id packing, engine.py:60-69).
+    * "philox" (default): per-thread Philox4x32-10 draws inside ONE
+      persistent kernel per batch of generations (csrc/generation.cu);
+      same operators and selection rule, different random numbers, no
+      host round trip per generation, populations up to 2^31 matrices.
+
+Fitness choices are the reference's "f1" and "f2" plus "sq" (sum of squared
+off-diagonal Gram entries); `evaluate` also returns "orth" (number of
+orthogonal column pairs), and `penalties` returns all four from one pass.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _dev
+from ._dev import HgaError, check, lib, ptr, stream_ptr, words_for
+from ._lib import FLAG_FIT_RANGE, FLAG_NOT_SIGN, FLAG_PLAN_RANGE, FLAG_POINT_RANGE, MUT_CODES, RunArgs, VARIANT_BITS
+from .rand import MASK64, RngStream, random_seed
+
+__all__ = [
+    "FITNESS_CHOICES",
+    "PENALTY_NAMES",
+    "MUTATION_STRATEGIES",
+    "RNG_MODES",
+    "MAX_ORDER",
+    "MAX_POPULATION",
+    "MAX_POPULATION_PHILOX",
+    "MAX_ITERATIONS",
+    "GAConfig",
+    "MutationPlan",
+    "SearchState",
+    "RunRecord",
+    "init_population",
+    "evaluate",
+    "penalties",
+    "select",
+    "draw_crossover_points",
+    "crossover",
+    "make_mutation_plan",
+    "mutate",
+    "initial_state",
+    "step",
+    "detect_stall",
+    "run_search",
+]
+
+FITNESS_CHOICES = ("f1", "f2", "sq")
+PENALTY_NAMES = ("f1", "f2", "orth", "sq")
+MUTATION_STRATEGIES = ("shared", "per-matrix", "multi")
+RNG_MODES = ("philox", "reference")
+
+_GEN_BITS, _MATRIX_BITS, _COL_BITS = 28, 20, 12
+MAX_ORDER = 1 << _COL_BITS
+MAX_POPULATION = (1 << _MATRIX_BITS) // 4       # reference-stream limit (engine.py:68)
+MAX_POPULATION_PHILOX = ((1 << 31) - 1) // 4     # 32-bit slot ids in the select keys
+MAX_ITERATIONS = (1 << _GEN_BITS) - 1
+MAX_RESIDENT_ORDER = 128                         # register-resident column words (W <= 4)
+
+_P_INIT, _P_SELECT, _P_CROSSOVER, _P_MUT_COL, _P_MUT_ROW_A, _P_MUT_ROW_B, _P_RESTART = 1, 2, 3, 4, 5, 6, 7
+
+DEBUG_CHECKS = False
+
+
+def _sid(purpose: int, generation: int = 0, matrix: int = 0, column: int = 0) -> int:
+    """Stream id packing (engine.py:84-90)."""
+    return (purpose << 60) | (generation << 32) | (matrix << 12) | column
+
+
+# ============================================================== config
+
+
+@dataclass(frozen=True)
+class GAConfig:
+    """All parameters of one search (engine.py:93-151) plus `rng`."""
+
+    order: int
+    population: int = 1000
+    max_iterations: int = 100_000
+    mutation_cols: int = 1
+    mutation_row_pairs: int = 2
+    fitness: str = "f2"
+    mutation: str = "multi"
+    seed: int | None = None
+    stall_window: int | None = None
+    time_budget_secs: float | None = None
+    rng: str = "philox"
+
+    def __post_init__(self):
+        m = self.order
+        if not isinstance(m, int) or m < 4 or m % 4 != 0:
+            raise ValueError(f"order must be a positive multiple of 4, got {m}")
+        if m > MAX_ORDER:
+            raise ValueError(f"order {m} exceeds engine limit {MAX_ORDER}")
+        if self.rng not in RNG_MODES:
+            raise ValueError(f"rng must be one of {RNG_MODES}")
+        cap = MAX_POPULATION if self.rng == "reference" else MAX_POPULATION_PHILOX
+        if not 1 <= self.population <= cap:
+            raise ValueError(f"population must be in [1, {cap}]")
+        if not 0 <= self.max_iterations <= MAX_ITERATIONS:
+            raise ValueError(f"max_iterations must be in [0, {MAX_ITERATIONS}]")
+        if not 1 <= self.mutation_cols <= m - 1:
+            raise ValueError(f"mutation_cols must be in [1, {m - 1}]")
+        if not 1 <= self.mutation_row_pairs <= m // 2:
+            raise ValueError(f"mutation_row_pairs must be in [1, {m // 2}]")
+        if self.fitness not in FITNESS_CHOICES:
+            raise ValueError(f"fitness must be one of {FITNESS_CHOICES}")
+        if self.mutation not in MUTATION_STRATEGIES:
+            raise ValueError(f"mutation must be one of {MUTATION_STRATEGIES}")
+        if self.seed is not None and not isinstance(self.seed, int):
+            raise ValueError("seed must be an integer or None")
+        if self.stall_window is not None and self.stall_window < 1:
+            raise ValueError("stall_window must be >= 1")
+        if self.time_budget_secs is not None and self.time_budget_secs <= 0:
+            raise ValueError("time_budget_secs must be positive")
+        if self.fitness == "sq" and m > 64:
+            raise ValueError("fitness 'sq' is limited to order <= 64 (24-bit selection keys)")
+
+    @property
+    def k(self) -> int:
+        return self.order // 4
+
+    @property
+    def parents(self) -> int:
+        return 2 * self.population
+
+    @property
+    def total(self) -> int:
+        return 4 * self.population
+
+
+# ============================================================== helpers
+
+
+def _is_numpy(a) -> bool:
+    return not isinstance(a, torch.Tensor)
+
+
+def _check_flag(flag: torch.Tensor, what: str) -> None:
+    v = int(flag.item())
+    if v & FLAG_NOT_SIGN:
+        raise ValueError(f"{what}: matrix entries must be +1 or -1")
+    if v & FLAG_POINT_RANGE:
+        raise IndexError(f"{what}: crossover point out of range")
+    if v & FLAG_PLAN_RANGE:
+        raise IndexError(f"{what}: mutation plan index out of range")
+    if v & FLAG_FIT_RANGE:
+        raise ValueError(f"{what}: fitness values span more than {int(lib.hga_select_max_range())}")
+
+
+def _pop_shape(pop) -> tuple[int, int]:
+    if pop.ndim != 3 or pop.shape[1] != pop.shape[2]:
+        raise ValueError(f"expected a (n, m, m) population, got shape {tuple(pop.shape)}")
+    return int(pop.shape[0]), int(pop.shape[1])
+
+
+def _copy_back(host: np.ndarray, dev: torch.Tensor) -> None:
+    host[...] = dev.cpu().numpy().reshape(host.shape)
+
+
+# ============================================================== fitness
+
+
+def _penalties_dev(pop: torch.Tensor, variants: int, check_sign: bool = True):
+    n, m = _pop_shape(pop)
+    dev = pop.device
+    outs = {}
+    for name, bit in VARIANT_BITS.items():
+        outs[name] = torch.empty(n, dtype=torch.int64, device=dev) if variants & bit else None
+    if n == 0:
+        return outs
+    flag = _dev.new_flag()
+    wsb = int(lib.hga_fitness_i8_ws_bytes(n, m))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
+    check(lib.hga_fitness_i8(pop.data_ptr(), n, m, variants, ptr(outs["f1"]), ptr(outs["f2"]), ptr(outs["orth"]),
+                             ptr(outs["sq"]), flag.data_ptr(), ptr(ws), wsb, stream_ptr()), "hga_fitness_i8")
+    if check_sign:
+        _check_flag(flag, "evaluate")
+    return outs
+
+
+def evaluate(population, fitness: str = "f2", workers: int = 1):
+    """Fitness vector aligned with `population` (engine.py:216-230).
+
+    numpy in -> numpy int64 out; CUDA int8 tensor in -> CUDA int64 tensor
+    out.  `workers` is accepted for signature compatibility: the GPU grid
+    replaces the reference's thread pool (results never depend on it).
+    """
+    if fitness not in PENALTY_NAMES:
+        raise ValueError(f"fitness must be one of {FITNESS_CHOICES} (or 'orth')")
+    host = _is_numpy(population)
+    pop, _ = _dev.to_device(population, torch.int8)
+    out = _penalties_dev(pop, VARIANT_BITS[fitness])[fitness]
+    return out.cpu().numpy() if host else out
+
+
+def penalties(population) -> dict:
+    """All four penalties (f1, f2, orth, sq) from one fused pass."""
+    host = _is_numpy(population)
+    pop, _ = _dev.to_device(population, torch.int8)
+    outs = _penalties_dev(pop, 15)
+    return {k: (v.cpu().numpy() if host else v) for k, v in outs.items()}
+
+
+# ============================================================== init
+
+
+def _init_packed(config: GAConfig, seed: int, purpose: int, generation: int, first_slot: int, count: int,
+                 out: torch.Tensor) -> None:
+    """Reference-stream balanced matrices into packed `out` (engine.py:154-182)."""
+    check(lib.hga_ref_init_packed(seed & MASK64, purpose, generation, first_slot, count, config.order,
+                                  out.data_ptr(), stream_ptr()), "hga_ref_init_packed")
+
+
+def _unpack(packed: torch.Tensor, n: int, m: int) -> torch.Tensor:
+    out = torch.empty((n, m, m), dtype=torch.int8, device=packed.device)
+    if n:
+        check(lib.hga_unpack_i8(packed.data_ptr(), n, m, out.data_ptr(), stream_ptr()), "hga_unpack_i8")
+    return out
+
+
+def _pack(pop: torch.Tensor) -> torch.Tensor:
+    n, m = _pop_shape(pop)
+    out = torch.empty(n * m * words_for(m), dtype=torch.int32, device=pop.device)
+    flag = _dev.new_flag()
+    if n:
+        check(lib.hga_pack_i8(pop.data_ptr(), n, m, out.data_ptr(), flag.data_ptr(), stream_ptr()), "hga_pack_i8")
+        _check_flag(flag, "pack")
+    return out
+
+
+def init_population_device(config: GAConfig, seed: int | None = None) -> torch.Tensor:
+    """(4N, m, m) int8 CUDA tensor of the initial population (reference streams)."""
+    if seed is None:
+        seed = config.seed
+    if seed is None:
+        raise ValueError("init_population needs an explicit seed")
+    dev = _dev.require_cuda()
+    m, total = config.order, config.total
+    out = torch.empty((total, m, m), dtype=torch.int8, device=dev)
+    if m <= MAX_RESIDENT_ORDER:
+        check(lib.hga_ref_init_i8(seed & MASK64, _P_INIT, 0, 0, total, m, out.data_ptr(), stream_ptr()),
+              "hga_ref_init_i8")
+        return out
+    packed = torch.empty(total * m * words_for(m), dtype=torch.int32, device=dev)
+    _init_packed(config, seed, _P_INIT, 0, 0, total, packed)
+    return _unpack(packed, total, m)
+
+
+def init_population(config: GAConfig, seed: int | None = None) -> np.ndarray:
+    """Initial population of 4N balanced matrices (engine.py:185-197), bit-identical
+    to the reference's for the same seed."""
+    return init_population_device(config, seed).cpu().numpy()
+
+
+# ============================================================== operators
+
+
+def select(population, fitness_values, stream) -> None:
+    """Move the 2N fittest into the parent slots in random order, in place
+    (engine.py:233-248; ties toward lower index; `stream` is an RngStream,
+    ours or the reference's, and advances by 2N-1 draws like the reference's).
+    """
+    half = population.shape[0] // 2
+    host_pop, host_fit = _is_numpy(population), _is_numpy(fitness_values)
+    pop, _ = _dev.to_device(population, torch.int8)
+    fit, _ = _dev.to_device(fitness_values, torch.int64)
+    if half == 0:
+        return
+    if not host_pop and pop.data_ptr() != population.data_ptr():
+        raise ValueError("device population must be a contiguous int8 tensor")
+    if not host_fit and fit.data_ptr() != fitness_values.data_ptr():
+        raise ValueError("device fitness must be a contiguous int64 tensor")
+    dev = pop.device
+    total = fit.shape[0]
+    order = torch.empty(half, dtype=torch.int64, device=dev)
+    wsb = int(lib.hga_select_ws_bytes(total))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    flag = _dev.new_flag()
+    check(lib.hga_select_order(fit.data_ptr(), total, order.data_ptr(), flag.data_ptr(), ws.data_ptr(), wsb,
+                               stream_ptr()), "hga_select_order")
+    _check_flag(flag, "select")
+    seed, sid, counter = int(stream.seed), int(stream.stream_id), int(stream.counter)
+    perm = torch.empty(half, dtype=torch.int64, device=dev)
+    pwsb = int(lib.hga_ref_permutation_ws_bytes(half))
+    pws = torch.empty(max(pwsb, 1), dtype=torch.uint8, device=dev)
+    check(lib.hga_ref_permutation(seed & MASK64, sid & MASK64, counter, half, perm.data_ptr(), pws.data_ptr(), pwsb,
+                                  stream_ptr()), "hga_ref_permutation")
+    stream.counter += half - 1
+    m = pop.shape[1]
+    tmp = torch.empty((half, m, m), dtype=torch.int8, device=dev)
+    ftmp = torch.empty(half, dtype=torch.int64, device=dev)
+    check(lib.hga_compose_gather(order.data_ptr(), perm.data_ptr(), half, pop.data_ptr(), tmp.data_ptr(), m * m,
+                                 fit.data_ptr(), ftmp.data_ptr(), None, stream_ptr()), "hga_compose_gather")
+    pop[:half].copy_(tmp)
+    fit[:half].copy_(ftmp)
+    if host_pop:
+        _copy_back(population, pop)
+    if host_fit:
+        _copy_back(fitness_values, fit)
+
+
+def draw_crossover_points(config: GAConfig, seed: int, generation: int) -> np.ndarray:
+    """One split column per parent pair, uniform in [1, m-1] (engine.py:251-254)."""
+    return RngStream(seed, _sid(_P_CROSSOVER, generation)).uniform_array(1, config.order - 1, config.population)
+
+
+def crossover(population, points) -> None:
+    """Rebuild all offspring from the parent pairs, in place (engine.py:257-277)."""
+    n_pairs = population.shape[0] // 4
+    m = population.shape[1]
+    pts_np = points.cpu().numpy() if isinstance(points, torch.Tensor) else np.asarray(points)
+    if pts_np.shape != (n_pairs,):
+        raise ValueError(f"expected {n_pairs} crossover points, got {pts_np.shape}")
+    if n_pairs and (pts_np.min() < 1 or pts_np.max() > m - 1):
+        raise IndexError(f"crossover points must lie in [1, {m - 1}]")
+    host = _is_numpy(population)
+    pop, _ = _dev.to_device(population, torch.int8)
+    pts, _ = _dev.to_device(pts_np.astype(np.int64), torch.int64)
+    flag = _dev.new_flag()
+    check(lib.hga_crossover_i8(pop.data_ptr(), pop.shape[0], m, pts.data_ptr(), flag.data_ptr(), stream_ptr()),
+          "hga_crossover_i8")
+    _check_flag(flag, "crossover")
+    if host:
+        _copy_back(population, pop)
+
+
+@dataclass(frozen=True)
+class MutationPlan:
+    """Flip targets for the 2N offspring (engine.py:280-302)."""
+
+    columns: np.ndarray
+    rows_a: np.ndarray
+    rows_b: np.ndarray
+
+    def __post_init__(self):
+        if self.columns.ndim != 2 or self.rows_a.ndim != 2 or self.rows_b.ndim != 2:
+            raise ValueError("plan arrays must be 2-D")
+        if self.rows_a.shape != self.rows_b.shape:
+            raise ValueError("row index arrays must have equal shapes")
+        if self.columns.shape[0] != self.rows_a.shape[0]:
+            raise ValueError("plan arrays must agree on offspring count")
+        if self.columns.size and self.columns.min() < 1:
+            raise IndexError("column 0 may not be mutated")
+
+
+def _plan_device(config: GAConfig, seed: int, generation: int):
+    """(cols, ra, rb) int64 CUDA tensors of the reference plan (engine.py:305-336)."""
+    m, n_off = config.order, config.parents
+    sc, sa, sb = _sid(_P_MUT_COL, generation), _sid(_P_MUT_ROW_A, generation), _sid(_P_MUT_ROW_B, generation)
+    from .rand import device_uniform
+
+    if config.mutation == "shared":
+        c = device_uniform(seed, sc, 0, 1, m - 1, 1)
+        a = device_uniform(seed, sa, 0, 0, m - 1, 1)
+        b = device_uniform(seed, sb, 0, 0, m - 1, 1)
+        return (c.expand(n_off).reshape(n_off, 1).contiguous(), a.expand(n_off).reshape(n_off, 1).contiguous(),
+                b.expand(n_off).reshape(n_off, 1).contiguous())
+    nc = 1 if config.mutation == "per-matrix" else config.mutation_cols
+    nr = 1 if config.mutation == "per-matrix" else config.mutation_row_pairs
+    return (device_uniform(seed, sc, 0, 1, m - 1, n_off * nc).reshape(n_off, nc),
+            device_uniform(seed, sa, 0, 0, m - 1, n_off * nr).reshape(n_off, nr),
+            device_uniform(seed, sb, 0, 0, m - 1, n_off * nr).reshape(n_off, nr))
+
+
+def make_mutation_plan(config: GAConfig, seed: int, generation: int) -> MutationPlan:
+    """Draw the mutation plan for one generation (engine.py:305-336)."""
+    c, a, b = _plan_device(config, seed, generation)
+    return MutationPlan(columns=c.cpu().numpy(), rows_a=a.cpu().numpy(), rows_b=b.cpu().numpy())
+
+
+def mutate(population, plan: MutationPlan) -> None:
+    """Apply the plan to the offspring half, in place (engine.py:339-373)."""
+    total, m = population.shape[0], population.shape[1]
+    half = total // 2
+    cols_np, ra_np, rb_np = (np.asarray(x) for x in (plan.columns, plan.rows_a, plan.rows_b))
+    n_off = cols_np.shape[0]
+    if n_off != half:
+        raise ValueError(f"plan covers {n_off} offspring, population has {half}")
+    if cols_np.size and cols_np.max() > m - 1:
+        raise IndexError(f"plan column beyond order {m}")
+    for arr in (ra_np, rb_np):
+        if arr.size and (arr.min() < 0 or arr.max() > m - 1):
+            raise IndexError("plan row index out of range")
+    host = _is_numpy(population)
+    pop, _ = _dev.to_device(population, torch.int8)
+    c, _ = _dev.to_device(cols_np.astype(np.int64), torch.int64)
+    a, _ = _dev.to_device(ra_np.astype(np.int64), torch.int64)
+    b, _ = _dev.to_device(rb_np.astype(np.int64), torch.int64)
+    flag = _dev.new_flag()
+    check(lib.hga_mutate_i8(pop.data_ptr(), total, m, c.data_ptr(), a.data_ptr(), b.data_ptr(), cols_np.shape[1],
+                            ra_np.shape[1], flag.data_ptr(), stream_ptr()), "hga_mutate_i8")
+    _check_flag(flag, "mutate")
+    if host:
+        _copy_back(population, pop)
+
+
+# ============================================================== search state
+
+
+@dataclass
+class RunRecord:
+    """Outcome of one search run (engine.py:390-402)."""
+
+    config: GAConfig
+    seed: int
+    success: bool
+    complete: bool
+    iterations: int
+    best_fitness: int
+    best_matrix: np.ndarray
+    trace: list[int]
+    wall_seconds: float
+
+
+class _Resident:
+    """Device side of a SearchState: packed ping-pong population + fitness."""
+
+    def __init__(self, config: GAConfig, seed: int):
+        self.config = config
+        self.seed = seed
+        self.dev = _dev.require_cuda()
+        m, N = config.order, config.population
+        self.m, self.N, self.W = m, N, words_for(m)
+        self.mw = m * self.W
+        total = 4 * N
+        self.pop = [torch.empty(total * self.mw, dtype=torch.int32, device=self.dev) for _ in range(2)]
+        self.fit = [torch.empty(total, dtype=torch.int64, device=self.dev) for _ in range(2)]
+        self.cur = 0
+        self.fit_var = VARIANT_BITS[config.fitness]
+        self.best_packed = torch.zeros(self.mw, dtype=torch.int32, device=self.dev)
+        self.dstate = torch.zeros(8, dtype=torch.int64, device=self.dev)
+        self.trace_dev = torch.zeros(1024, dtype=torch.int64, device=self.dev)
+        self.key = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.run_ws = None
+        self.sel_ws = None
+        self.perm_ws = None
+
+    # -- argmin over a fitness buffer, lowest index on ties
+    def argmin(self, fit: torch.Tensor) -> tuple[int, int]:
+        check(lib.hga_argmin_key(fit.data_ptr(), fit.shape[0], self.key.data_ptr(), 1, stream_ptr()), "argmin")
+        k = int(self.key.item()) & MASK64
+        return k >> 32, k & 0xFFFFFFFF
+
+    def matrix(self, buf: int, idx: int) -> torch.Tensor:
+        return self.pop[buf][idx * self.mw:(idx + 1) * self.mw]
+
+    def run_args(self) -> RunArgs:
+        cfg = self.config
+        if self.run_ws is None:
+            wsb = int(lib.hga_run_ws_bytes(self.N, self.m))
+            self.run_ws = torch.zeros(wsb, dtype=torch.uint8, device=self.dev)
+        a = RunArgs()
+        a.pop[0], a.pop[1] = self.pop[0].data_ptr(), self.pop[1].data_ptr()
+        a.fit[0], a.fit[1] = self.fit[0].data_ptr(), self.fit[1].data_ptr()
+        a.n_pairs, a.m = self.N, self.m
+        a.nc, a.nr = cfg.mutation_cols, cfg.mutation_row_pairs
+        a.strategy = MUT_CODES[cfg.mutation]
+        a.fit_var = self.fit_var
+        a.stall_window = cfg.stall_window or 0
+        a.seed = self.seed & MASK64
+        a.max_generation = cfg.max_iterations
+        a.gens_this_call = 0
+        a.state = self.dstate.data_ptr()
+        a.trace = self.trace_dev.data_ptr()
+        a.trace_capacity = self.trace_dev.shape[0]
+        a.best_matrix = self.best_packed.data_ptr()
+        a.ws = self.run_ws.data_ptr()
+        a.ws_bytes = self.run_ws.shape[0]
+        return a
+
+    def ensure_trace(self, upto: int) -> None:
+        cap = self.trace_dev.shape[0]
+        if upto < cap:
+            return
+        new = max(upto + 1, 2 * cap)
+        t = torch.zeros(new, dtype=torch.int64, device=self.dev)
+        t[:cap].copy_(self.trace_dev)
+        self.trace_dev = t
+
+
+class SearchState:
+    """Mutable state of a running search (engine.py:376-387).
+
+    The population lives on the GPU (packed); `population`, `fitness` and
+    `best_matrix` materialise reference-layout numpy copies on access.
+    """
+
+    def __init__(self, config: GAConfig, seed: int, res: _Resident, iteration: int, best_fitness: int,
+                 trace: list[int], best_matrix: np.ndarray):
+        self.config = config
+        self.seed = seed
+        self._res = res
+        self.iteration = iteration
+        self.best_fitness = best_fitness
+        self.trace = trace
+        self.best_matrix = best_matrix
+        self._last_restart = 0
+
+    @property
+    def population(self) -> np.ndarray:
+        r = self._res
+        return _unpack(r.pop[r.cur], 4 * r.N, r.m).cpu().numpy()
+
+    @property
+    def population_device(self) -> torch.Tensor:
+        r = self._res
+        return _unpack(r.pop[r.cur], 4 * r.N, r.m)
+
+    @property
+    def packed_population(self) -> torch.Tensor:
+        r = self._res
+        return r.pop[r.cur].view(4 * r.N, r.m, r.W)
+
+    @property
+    def fitness(self) -> np.ndarray:
+        r = self._res
+        return r.fit[r.cur].cpu().numpy()
+
+    @property
+    def fitness_device(self) -> torch.Tensor:
+        r = self._res
+        return r.fit[r.cur]
+
+
+def _best_from_packed(res: _Resident, packed: torch.Tensor) -> np.ndarray:
+    return _unpack(packed, 1, res.m)[0].cpu().numpy()
+
+
+def initial_state(config: GAConfig, seed: int | None = None, workers: int = 1) -> SearchState:
+    """Initialise and evaluate the full population (engine.py:405-428)."""
+    if seed is None:
+        seed = config.seed if config.seed is not None else random_seed()
+    seed &= MASK64
+    if config.order > MAX_RESIDENT_ORDER:
+        raise HgaError(f"resident GA supports order <= {MAX_RESIDENT_ORDER}")
+    res = _Resident(config, seed)
+    m, total = config.order, config.total
+    if config.rng == "reference":
+        _init_packed(config, seed, _P_INIT, 0, 0, total, res.pop[0])
+        fvar = res.fit_var
+        out = res.fit[0]
+        check(lib.hga_fitness_packed(res.pop[0].data_ptr(), total, m, fvar, ptr(out) if fvar == 1 else None,
+                                     ptr(out) if fvar == 2 else None, None, ptr(out) if fvar == 8 else None,
+                                     stream_ptr()), "hga_fitness_packed")
+        best, idx = res.argmin(res.fit[0])
+        res.best_packed.copy_(res.matrix(0, idx))
+        res.dstate.copy_(torch.tensor([0, best, 0, 0, idx, int(best == 0), 1, best], dtype=torch.int64))
+    else:
+        a = res.run_args()
+        check(lib.hga_run_init(a, stream_ptr()), "hga_run_init")
+        st = res.dstate.cpu().tolist()
+        best = int(st[1])
+    return SearchState(config, seed, res, 0, int(best), [int(best)], _best_from_packed(res, res.best_packed))
+
+
+def _step_reference(state: SearchState) -> None:
+    res, cfg = state._res, state.config
+    gen = state.iteration + 1
+    N, m, half, total = res.N, res.m, 2 * res.N, 4 * res.N
+    cur, nxt = res.cur, res.cur ^ 1
+    dev = res.dev
+    sp = stream_ptr()
+    # select (engine.py:233-248): stable order, reference permutation, gather
+    order = torch.empty(half, dtype=torch.int64, device=dev)
+    if res.sel_ws is None:
+        wsb = int(lib.hga_select_ws_bytes(total))
+        res.sel_ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        pwsb = int(lib.hga_ref_permutation_ws_bytes(half))
+        res.perm_ws = torch.empty(max(pwsb, 1), dtype=torch.uint8, device=dev)
+    flag = _dev.new_flag()
+    check(lib.hga_select_order(res.fit[cur].data_ptr(), total, order.data_ptr(), flag.data_ptr(),
+                               res.sel_ws.data_ptr(), res.sel_ws.shape[0], sp), "hga_select_order")
+    perm = torch.empty(half, dtype=torch.int64, device=dev)
+    check(lib.hga_ref_permutation(state.seed, _sid(_P_SELECT, gen), 0, half, perm.data_ptr(), res.perm_ws.data_ptr(),
+                                  res.perm_ws.shape[0], sp), "hga_ref_permutation")
+    check(lib.hga_compose_gather(order.data_ptr(), perm.data_ptr(), half, res.pop[cur].data_ptr(),
+                                 res.pop[nxt].data_ptr(), res.mw * 4, res.fit[cur].data_ptr(), res.fit[nxt].data_ptr(),
+                                 None, sp), "hga_compose_gather")
+    # crossover points + mutation plan (reference streams), fused generation
+    from .rand import device_uniform
+
+    points = device_uniform(state.seed, _sid(_P_CROSSOVER, gen), 0, 1, m - 1, N)
+    cols, ra, rb = _plan_device(cfg, state.seed, gen)
+    check(lib.hga_generation_explicit(res.pop[nxt].data_ptr(), res.fit[nxt].data_ptr(), N, m, points.data_ptr(),
+                                      cols.data_ptr(), ra.data_ptr(), rb.data_ptr(), cols.shape[1], ra.shape[1],
+                                      res.fit_var, None, sp), "hga_generation_explicit")
+    res.cur = nxt
+    fmin, idx = res.argmin(res.fit[nxt])
+    _check_flag(flag, "select")
+    state.iteration = gen
+    state.trace.append(fmin)
+    if fmin < state.best_fitness:
+        state.best_fitness = fmin
+        res.best_packed.copy_(res.matrix(nxt, idx))
+        state.best_matrix = _best_from_packed(res, res.best_packed)
+
+
+def _sync_from_device(state: SearchState) -> None:
+    """Pull the 8-word device state + new trace entries after hga_run."""
+    res = state._res
+    st = res.dstate.cpu().tolist()
+    it = int(st[0])
+    if it > state.iteration:
+        state.trace.extend(int(v) for v in res.trace_dev[state.iteration + 1:it + 1].cpu().tolist())
+    improved = int(st[1]) < state.best_fitness
+    state.iteration = it
+    state.best_fitness = int(st[1])
+    state._last_restart = int(st[2])
+    res.cur = int(st[3])
+    if improved:
+        state.best_matrix = _best_from_packed(res, res.best_packed)
+
+
+def _run_device(state: SearchState, gens: int) -> None:
+    res = state._res
+    res.ensure_trace(state.iteration + gens)
+    a = res.run_args()
+    a.gens_this_call = gens
+    check(lib.hga_run(a, stream_ptr()), "hga_run")
+    _sync_from_device(state)
+
+
+def step(state: SearchState, workers: int = 1) -> SearchState:
+    """Advance one generation (engine.py:449-469)."""
+    if state.config.rng == "reference":
+        _step_reference(state)
+    else:
+        cfg = state.config
+        # one generation, ignoring the loop's own stop conditions
+        res = state._res
+        res.dstate[5] = 0
+        saved = cfg.max_iterations
+        a_cap = max(saved, state.iteration + 1)
+        res.ensure_trace(state.iteration + 1)
+        a = res.run_args()
+        a.max_generation = a_cap
+        a.stall_window = 0
+        a.gens_this_call = 1
+        check(lib.hga_run(a, stream_ptr()), "hga_run")
+        _sync_from_device(state)
+    if DEBUG_CHECKS:
+        _check_state(state)
+    return state
+
+
+def _check_state(state: SearchState) -> None:
+    pop = state.population
+    assert (pop[:, :, 0] == 1).all(), "first column lost its all-+1 contract"
+    assert (pop[:, :, 1:].sum(axis=1, dtype=np.int64) == 0).all(), "column balance broken"
+    assert np.array_equal(state.fitness, evaluate(pop, state.config.fitness)), "fitness vector is stale"
+
+
+def detect_stall(state: SearchState, window: int) -> bool:
+    """True when the min-fitness trace sat flat and positive for `window` steps (engine.py:472-479)."""
+    if window < 1:
+        raise ValueError("window must be >= 1")
+    tail = state.trace[-window:]
+    if len(tail) < window or tail[-1] == 0:
+        return False
+    return all(v == tail[0] for v in tail)
+
+
+def _reinitialize_offspring(state: SearchState) -> None:
+    """Fresh balanced offspring, parents retained (engine.py:482-494), reference streams."""
+    res, cfg = state._res, state.config
+    half, total, m = 2 * res.N, 4 * res.N, res.m
+    cur = res.cur
+    off = res.pop[cur][half * res.mw:]
+    _init_packed(cfg, state.seed, _P_RESTART, state.iteration, half, half, off)
+    fo = res.fit[cur][half:]
+    fv = res.fit_var
+    check(lib.hga_fitness_packed(off.data_ptr(), half, m, fv, ptr(fo) if fv == 1 else None,
+                                 ptr(fo) if fv == 2 else None, None, ptr(fo) if fv == 8 else None, stream_ptr()),
+          "hga_fitness_packed")
+    fmin, idx = res.argmin(res.fit[cur][:total])
+    if fmin < state.best_fitness:
+        state.best_fitness = fmin
+        res.best_packed.copy_(res.matrix(cur, idx))
+        state.best_matrix = _best_from_packed(res, res.best_packed)
+
+
+def run_search(config: GAConfig, workers: int = 1, poll_interval: int = 256) -> RunRecord:
+    """Init, then step until fitness 0 or budgets run out (engine.py:497-538).
+
+    Philox mode runs `poll_interval` generations per kernel launch (the
+    device stops by itself on success or max_iterations; the host only
+    reads an 8-word state block between launches for the time budget).
+    """
+    start = time.perf_counter()
+    state = initial_state(config, workers=workers)
+    complete = True
+    if config.rng == "reference":
+        last_restart = 0
+        while state.iteration < config.max_iterations and state.best_fitness > 0:
+            if config.time_budget_secs is not None and time.perf_counter() - start > config.time_budget_secs:
+                complete = False
+                break
+            step(state)
+            if (config.stall_window is not None and state.best_fitness > 0
+                    and state.iteration - last_restart >= config.stall_window
+                    and detect_stall(state, config.stall_window)):
+                _reinitialize_offspring(state)
+                last_restart = state.iteration
+    else:
+        while state.iteration < config.max_iterations and state.best_fitness > 0:
+            if config.time_budget_secs is not None and time.perf_counter() - start > config.time_budget_secs:
+                complete = False
+                break
+            gens = min(poll_interval, config.max_iterations - state.iteration)
+            _run_device(state, gens)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - start
+    success = state.best_fitness == 0
+    return RunRecord(config=config, seed=state.seed, success=success, complete=complete or success,
+                     iterations=state.iteration, best_fitness=state.best_fitness, best_matrix=state.best_matrix,
+                     trace=list(state.trace), wall_seconds=wall)

@@ -1,0 +1,299 @@
+"""CUDA path vs the oracle and the reference's golden vectors (B200 only).
+
+Bit-exact is the bar everywhere: fitness values, stream draws, init,
+select/crossover/mutate results, and -- in reference-stream mode -- whole
+RunRecords (trace, iteration count, best matrix) of the reference itself.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import run_config
+
+pytestmark = pytest.mark.gpu
+
+hga = pytest.importorskip("paper_2208_14961_b200")
+from paper_2208_14961_b200 import engine  # noqa: E402
+from paper_2208_14961_b200.rand import RngStream  # noqa: E402
+
+
+# ------------------------------------------------------------------ fitness
+
+
+def test_fitness_golden_all_cases(golden, cuda_device):
+    for name in golden["fit_names"]:
+        pop = golden[f"fit_pop_{name}"]
+        want = golden[f"fit_val_{name}"]
+        got = hga.penalties(pop)
+        for col, key in enumerate(("f1", "f2", "orth", "sq")):
+            assert np.array_equal(got[key], want[:, col]), (name, key)
+        for col, key in enumerate(("f1", "f2", "orth", "sq")):
+            assert np.array_equal(hga.evaluate(pop, key), want[:, col]), (name, key)
+
+
+@pytest.mark.parametrize("m", [4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 64, 96, 100, 128, 132, 200])
+def test_fitness_random_vs_oracle(m, cuda_device):
+    rng = np.random.default_rng(1000 + m)
+    n = 300 if m <= 64 else 24
+    bal = oracle.random_balanced(m, n, 77 + m, 1, 0, 0)
+    unb = rng.choice(np.array([-1, 1], dtype=np.int8), size=(n // 3, m, m))
+    for pop in (bal, unb):
+        want = oracle.penalties(pop, threads=4)
+        got = hga.penalties(pop)
+        for col, key in enumerate(("f1", "f2", "orth", "sq")):
+            assert np.array_equal(got[key], want[:, col]), (m, key)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 6, 7, 9, 10, 13, 31, 33, 63, 65, 127, 129])
+def test_fitness_odd_and_unaligned_orders(m, cuda_device):
+    rng = np.random.default_rng(m)
+    pop = rng.choice(np.array([-1, 1], dtype=np.int8), size=(37, m, m))
+    want = oracle.penalties(pop)
+    got = hga.penalties(pop)
+    for col, key in enumerate(("f1", "f2", "orth", "sq")):
+        assert np.array_equal(got[key], want[:, col]), (m, key)
+
+
+def test_fitness_device_tensor_and_empty(cuda_device):
+    pop = oracle.random_balanced(20, 50, 5, 1, 0, 0)
+    t = torch.from_numpy(pop).cuda()
+    out = hga.evaluate(t, "f1")
+    assert out.is_cuda and out.dtype == torch.int64
+    assert np.array_equal(out.cpu().numpy(), oracle.evaluate(pop, "f1"))
+    assert hga.evaluate(np.zeros((0, 12, 12), np.int8), "f2").shape == (0,)
+
+
+def test_fitness_rejects_non_sign(cuda_device):
+    pop = np.ones((3, 12, 12), dtype=np.int8)
+    pop[1, 4, 7] = 0
+    with pytest.raises(ValueError):
+        hga.evaluate(pop, "f2")
+    pop[1, 4, 7] = 3
+    with pytest.raises(ValueError):
+        hga.evaluate(pop, "f1")
+    with pytest.raises(ValueError):
+        hga.evaluate(np.ones((2, 4, 4), np.int8), "f3")
+
+
+def test_fitness_large_population_sampled(cuda_device):
+    m, n = 20, 1_000_000
+    pop_t = engine.init_population_device(engine.GAConfig(order=m, population=n // 4, seed=2024, rng="reference"))
+    got = hga.evaluate(pop_t, "f2").cpu().numpy()
+    idx = np.random.default_rng(0).choice(n, 2000, replace=False)
+    sample = pop_t[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert np.array_equal(got[idx], oracle.evaluate(sample, "f2"))
+    # size-independent properties on the whole batch
+    assert (got >= 0).all() and (got % 2 == 0).all()
+
+
+def test_pack_unpack_roundtrip(cuda_device):
+    for m in (4, 12, 20, 33, 64, 100, 130):
+        pop = np.random.default_rng(m).choice(np.array([-1, 1], dtype=np.int8), size=(17, m, m))
+        t = torch.from_numpy(pop).cuda()
+        packed = engine._pack(t)
+        back = engine._unpack(packed, 17, m).cpu().numpy()
+        assert np.array_equal(back, pop), m
+        pf = torch.empty(17, dtype=torch.int64, device="cuda")
+        hga._lib.lib.hga_fitness_packed(packed.data_ptr(), 17, m, 2, None, pf.data_ptr(), None, None,
+                                        torch.cuda.current_stream().cuda_stream)
+        assert np.array_equal(pf.cpu().numpy(), oracle.evaluate(pop, "f2")), m
+
+
+# ------------------------------------------------------------------ streams
+
+
+def test_reference_streams(golden, cuda_device):
+    for a, s in enumerate(golden["rng_seeds"][:3]):
+        w = torch.empty(64, dtype=torch.int64, device="cuda")
+        hga._lib.lib.hga_ref_words(int(s), 17, 5, 64, w.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        assert np.array_equal(w.cpu().numpy().view(np.uint64), golden["rng_words_seed_sid17_c5"][a])
+    assert np.array_equal(RngStream(99, 12).uniform_array(1, 11, 1000), golden["rng_uniform_99_12_1_11"])
+    assert np.array_equal(RngStream(7, 3, counter=11).uniform_array(0, 35, 333), golden["rng_uniform_7_3_0_35"])
+    for n in (1, 2, 5, 100, 1000, 4097):
+        st = RngStream(3, engine._sid(2, 9), counter=2)
+        assert np.array_equal(st.permutation(n), golden[f"rng_perm_{n}"]), n
+        assert st.counter == 2 + n - 1
+
+
+def test_permutation_large_matches_oracle(cuda_device):
+    for n in (50_000, 60_000, 200_001):
+        got = RngStream(11, 5, counter=3).permutation(n)
+        assert np.array_equal(got, oracle.permutation(11, 5, 3, n)), n
+
+
+@pytest.mark.parametrize("m", [4, 8, 12, 20, 36, 64])
+def test_init_golden(golden, m, cuda_device):
+    mm, count, seed, purpose, gen, first = [int(v) for v in golden[f"init_m{m}_args"]]
+    cfg = engine.GAConfig(order=m, population=1, rng="reference")
+    packed = torch.empty(count * m * ((m + 31) // 32), dtype=torch.int32, device="cuda")
+    engine._init_packed(cfg, seed, purpose, gen, first, count, packed)
+    assert np.array_equal(engine._unpack(packed, count, m).cpu().numpy(), golden[f"init_m{m}"])
+
+
+def test_init_population_matches_oracle(cuda_device):
+    for m, n_pairs, seed in [(12, 100, 3), (20, 250, 2024), (36, 10, 9), (128, 2, 1), (132, 1, 4)]:
+        cfg = engine.GAConfig(order=m, population=n_pairs, seed=seed, rng="reference")
+        assert np.array_equal(hga.init_population(cfg), oracle.init_population(m, n_pairs, seed)), m
+
+
+# ------------------------------------------------------------------ operators
+
+
+@pytest.mark.parametrize("m", [8, 12, 20])
+def test_select_golden(golden, m, cuda_device):
+    tag = f"select_m{m}"
+    _, _, seed, gen = [int(v) for v in golden[f"{tag}_args"]]
+    pop = golden[f"{tag}_pop_in"].copy()
+    fit = golden[f"{tag}_fit_in"].copy()
+    st = RngStream(seed, engine._sid(2, gen))
+    hga.select(pop, fit, st)
+    assert np.array_equal(pop, golden[f"{tag}_pop_out"])
+    assert np.array_equal(fit, golden[f"{tag}_fit_out"])
+    assert st.counter == int(golden[f"{tag}_counter_after"][0])
+
+
+def test_select_device_ties_and_large(cuda_device):
+    rng = np.random.default_rng(3)
+    for total, m, spread in [(4000, 12, 3), (40_000, 20, 50), (400, 8, 1)]:
+        pop = oracle.random_balanced(m, total, 5, 1, 0, 0)
+        fit = rng.integers(0, spread, size=total).astype(np.int64) * 4 + 100
+        want_p, want_f = pop.copy(), fit.copy()
+        oracle.select(want_p, want_f, 9, engine._sid(2, 3))
+        tp, tf = torch.from_numpy(pop).cuda(), torch.from_numpy(fit).cuda()
+        hga.select(tp, tf, RngStream(9, engine._sid(2, 3)))
+        assert np.array_equal(tp.cpu().numpy(), want_p)
+        assert np.array_equal(tf.cpu().numpy(), want_f)
+
+
+@pytest.mark.parametrize("m", [8, 12, 20, 36])
+def test_crossover_mutation_golden(golden, m, cuda_device):
+    tag = f"xo_m{m}"
+    _, n_pairs, seed, gen, nc, nr = [int(v) for v in golden[f"{tag}_args"]]
+    cfg = engine.GAConfig(order=m, population=n_pairs, seed=seed, mutation_cols=nc, mutation_row_pairs=nr,
+                          rng="reference")
+    pts = hga.draw_crossover_points(cfg, seed, gen)
+    assert np.array_equal(pts, golden[f"{tag}_points"])
+    pop = golden[f"{tag}_pop_in"].copy()
+    hga.crossover(pop, pts)
+    assert np.array_equal(pop, golden[f"{tag}_pop_out"])
+    for strat in ("shared", "per-matrix", "multi"):
+        s = strat.replace("-", "_")
+        scfg = engine.GAConfig(order=m, population=n_pairs, seed=seed, mutation_cols=nc, mutation_row_pairs=nr,
+                               mutation=strat, rng="reference")
+        plan = hga.make_mutation_plan(scfg, seed, gen)
+        assert np.array_equal(plan.columns, golden[f"{tag}_plan_{s}_cols"])
+        assert np.array_equal(plan.rows_a, golden[f"{tag}_plan_{s}_ra"])
+        assert np.array_equal(plan.rows_b, golden[f"{tag}_plan_{s}_rb"])
+        mt = pop.copy()
+        hga.mutate(mt, plan)
+        assert np.array_equal(mt, golden[f"{tag}_mut_{s}"]), strat
+
+
+def test_operator_errors(cuda_device):
+    pop = oracle.init_population(8, 2, 1)
+    with pytest.raises(ValueError):
+        hga.crossover(pop, np.array([1, 2, 3]))
+    with pytest.raises(IndexError):
+        hga.crossover(pop, np.array([0, 3]))
+    with pytest.raises(IndexError):
+        hga.crossover(pop, np.array([3, 8]))
+    plan = engine.MutationPlan(np.ones((4, 1), np.int64), np.zeros((4, 1), np.int64), np.zeros((4, 1), np.int64))
+    with pytest.raises(ValueError):
+        hga.mutate(oracle.init_population(8, 3, 1), plan)
+    with pytest.raises(IndexError):
+        engine.MutationPlan(np.zeros((4, 1), np.int64), np.zeros((4, 1), np.int64), np.zeros((4, 1), np.int64))
+    bad = engine.MutationPlan(np.full((4, 1), 8, np.int64), np.zeros((4, 1), np.int64), np.zeros((4, 1), np.int64))
+    with pytest.raises(IndexError):
+        hga.mutate(pop, bad)
+
+
+def test_figure2_crossover(golden, cuda_device):
+    par = golden["fig2_parents"]
+    pop = np.concatenate([par, np.zeros_like(par)])
+    hga.crossover(pop, np.array([3]))
+    assert np.array_equal(pop[2:], golden["fig2_offspring"])
+
+
+# ------------------------------------------------------------------ whole loop, reference streams
+
+
+def test_reference_mode_state_after_three_steps(golden, cuda_device):
+    for i in range(int(golden["run_count"][0])):
+        kw = run_config(golden, i)
+        cfg = engine.GAConfig(**kw, rng="reference")
+        st = hga.initial_state(cfg)
+        for _ in range(min(3, kw["max_iterations"])):
+            hga.step(st)
+        assert np.array_equal(st.population, golden[f"run{i}_state3_pop"]), i
+        assert np.array_equal(st.fitness, golden[f"run{i}_state3_fit"]), i
+
+
+def test_reference_mode_run_records(golden, cuda_device):
+    for i in range(int(golden["run_count"][0])):
+        kw = run_config(golden, i)
+        rec = hga.run_search(engine.GAConfig(**kw, rng="reference"))
+        it, best, succ = golden[f"run{i}_meta"].tolist()
+        assert rec.trace == golden[f"run{i}_trace"].tolist(), i
+        assert (rec.iterations, rec.best_fitness, int(rec.success)) == (it, best, succ), i
+        assert np.array_equal(rec.best_matrix, golden[f"run{i}_best"]), i
+
+
+# ------------------------------------------------------------------ production (Philox) loop
+
+
+def _invariants(st):
+    pop = st.population
+    assert (pop[:, :, 0] == 1).all()
+    assert (pop[:, :, 1:].sum(axis=1, dtype=np.int64) == 0).all()
+    assert np.array_equal(st.fitness, oracle.evaluate(pop, st.config.fitness))
+
+
+@pytest.mark.parametrize("m,fit", [(12, "f2"), (20, "f1"), (28, "f2"), (36, "f1"), (64, "f2"), (16, "sq")])
+def test_philox_steps_keep_invariants(m, fit, cuda_device):
+    cfg = engine.GAConfig(order=m, population=300, seed=11, fitness=fit, mutation_cols=2, mutation_row_pairs=3)
+    st = hga.initial_state(cfg)
+    _invariants(st)
+    prev = st.trace[-1]
+    for _ in range(5):
+        hga.step(st)
+        _invariants(st)
+        assert st.trace[-1] <= prev
+        prev = st.trace[-1]
+        assert st.trace[-1] == int(st.fitness.min())
+    assert len(st.trace) == 6
+
+
+def test_philox_parents_are_the_selected_set(cuda_device):
+    cfg = engine.GAConfig(order=20, population=500, seed=4, fitness="f2")
+    st = hga.initial_state(cfg)
+    before_pop, before_fit = st.population, st.fitness
+    hga.step(st)
+    after = st.population
+    half = 2 * cfg.population
+    order = np.argsort(before_fit, kind="stable")[:half]
+    want = {before_pop[i].tobytes() for i in order}
+    got = [after[s].tobytes() for s in range(half)]
+    assert sorted(got) == sorted(before_pop[i].tobytes() for i in order)
+    assert set(got) == want
+    assert np.array_equal(np.sort(st.fitness[:half]), np.sort(before_fit[order]))
+
+
+def test_philox_search_finds_and_verifies(cuda_device):
+    for m in (8, 12, 16):
+        rec = hga.run_search(engine.GAConfig(order=m, population=1000, seed=5, fitness="f1", max_iterations=3000))
+        assert rec.success, m
+        assert oracle.penalties(rec.best_matrix[None])[0, 1] == 0
+        assert hga.core.is_hadamard(rec.best_matrix)
+        assert all(a >= b for a, b in zip(rec.trace, rec.trace[1:]))
+        assert rec.trace[-1] == 0 and len(rec.trace) == rec.iterations + 1
+
+
+def test_philox_stall_restart_runs(cuda_device):
+    cfg = engine.GAConfig(order=16, population=50, seed=2, fitness="f2", max_iterations=300, stall_window=5)
+    rec = hga.run_search(cfg)
+    assert all(a >= b for a, b in zip(rec.trace, rec.trace[1:]))
+    assert rec.best_fitness == rec.trace[-1] or rec.best_fitness <= rec.trace[-1]
