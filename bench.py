@@ -1,0 +1,409 @@
+"""Benchmark of the GA inner loop (BASELINE.json metric: matrix fitness evals/s).
+
+Workload (BASELINE.json configs[1]): order-20 GA, population 40,000 matrices
+(N = 10,000 pairs), on one B200 per rank.  One step = one generation:
+select over all 4N -> column-block crossover -> +-1 pair-flip mutation ->
+fitness of the 2N offspring (engine.py:449-469), i.e. 2N = 20,000 matrix
+fitness evaluations per step per GPU.  Fitness F2 (the reference default),
+mutation "multi" with NC=4, NR=2 (the reference's own bench setting,
+bench.py:264-273 of hadamard_ga); Philox streams.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value`  device-timed throughput: per-step CUDA events around the one
+         persistent-kernel launch of that generation, L2 flushed (256 MiB
+         write) between steps outside the events; max over ranks.
+`e2e`    the same metric through the public drop-in API with HOST buffers:
+         engine.step() on a reference-style state whose population/fitness
+         are numpy arrays -> H2D of the int8 population + fitness, the
+         generation, D2H of both, every step (wall clock).
+`roofline` the generation kernel (k_run) against the measured HBM peak with
+         its algorithmic bytes; `fitness_sweep`
+         adds the large-batch fitness kernel (config 5) at m = 20..64.
+`cpu_baseline` the C oracle port (oracle/hga_oracle.c) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+ORDER, N_PAIRS, FITNESS, NC, NR = 20, 10_000, "f2", 4, 2
+METRIC = "matrix fitness evals/sec (order-20 GA generation, 40,000 matrices, 2N offspring evaluated per generation)"
+UNIT = "evals/s"
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, ValueError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def algorithmic_bytes_per_generation(m: int, n_pairs: int) -> int:
+    """Minimum HBM traffic of one generation:
+    read 4N fitness (selection), read the 2N selected parents, write the new
+    population (2N parent copies + 2N offspring) and its 4N fitness."""
+    mat = 4 * m * ((m + 31) // 32)
+    total = 4 * n_pairs
+    return total * 8 + 2 * n_pairs * mat + total * mat + total * 8
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    import paper_2208_14961_b200 as hga
+    from paper_2208_14961_b200 import engine
+    from paper_2208_14961_b200._lib import RUN_FORCE, lib, check
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    cfg = engine.GAConfig(order=ORDER, population=N_PAIRS, seed=2024 + rank, fitness=FITNESS, mutation_cols=NC,
+                          mutation_row_pairs=NR, max_iterations=engine.MAX_ITERATIONS)
+    st = hga.initial_state(cfg)
+    res = st._res
+    res.ensure_trace(args.warmup + args.steps + 8)
+    a = res.run_args()
+    a.gens_this_call = 1
+    a.flags = RUN_FORCE
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def one_generation():
+        check(lib.hga_run(a, sp), "hga_run")
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        one_generation()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    wall0 = time.perf_counter()
+    for s, e in evs:
+        flush.fill_(1)  # write 256 MiB > 126 MB L2 between timed steps
+        s.record(stream)
+        one_generation()
+        e.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+    step_s = [s.elapsed_time(e) / 1e3 for s, e in evs]
+    t_total = sum(step_s)
+    if dist:
+        tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total = float(tt.item())
+    per_step = t_total / args.steps
+    evals_per_step = 2 * N_PAIRS
+    value = evals_per_step * world / per_step
+
+    # roofline of the dominant (only) kernel of the step: k_run
+    alg_bytes = algorithmic_bytes_per_generation(ORDER, N_PAIRS)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = alg_bytes / per_step / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "k_run (one generation, persistent cooperative kernel)",
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
+                "popc_ceiling_evals_per_s": 4.52e12 / (ORDER * (ORDER - 1) // 2)}
+    prof = ROOT / "profiles" / "r01_k_run_traffic.json"
+    if prof.exists():
+        try:
+            roofline["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except (ValueError, OSError):
+            pass
+
+    # production mode: K generations back to back in ONE launch (no flush)
+    a2 = res.run_args()
+    a2.gens_this_call = args.steps
+    a2.flags = RUN_FORCE
+    res.ensure_trace(st.iteration + 2 * args.steps + 2 * args.warmup + 16)
+    a2 = res.run_args()
+    a2.gens_this_call = args.steps
+    a2.flags = RUN_FORCE
+    s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    check(lib.hga_run(a2, sp), "hga_run")
+    e0.record(stream)
+    torch.cuda.synchronize()
+    persistent = evals_per_step * args.steps / (s0.elapsed_time(e0) / 1e3)
+
+    # e2e through the public API with host (numpy) buffers
+    e2e = run_e2e(args, cfg, hga, engine, torch)
+
+    # fitness-only sweep (config 5) at large n: the kernel's own roofline
+    sweep = run_fitness_sweep(args, engine, torch, lib, peak) if not args.no_sweep else None
+
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": per_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32 bit-packed +-1 (int64 fitness)",
+        "data": "synthetic: Philox-seeded random balanced sign matrices (seed 2024 + rank)",
+        "config": {"workload": "BASELINE configs[1]: order-20 GA, population 40,000 matrices (N=10,000 pairs), "
+                               "fitness f2, mutation multi NC=4 NR=2, rng philox",
+                   "order": ORDER, "matrices": 4 * N_PAIRS, "offspring_evals_per_step": evals_per_step,
+                   "parallelism": f"islands x{world} (one independent population per GPU)",
+                   "l2": "flushed between timed steps (256 MiB write, outside the CUDA events)"},
+        "gpu_launches": args.steps,
+        "roofline": roofline,
+        "e2e": e2e,
+        "persistent_run": {"value": persistent * world, "unit": UNIT, "generations_per_launch": args.steps,
+                           "note": "production run_search mode: K generations in one launch, L2 warm"},
+        "wall_seconds_timed_region": wall,
+        "clocks": clocks,
+    }
+    if sweep:
+        out["fitness_sweep"] = sweep
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(args)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_e2e(args, cfg, hga, engine, torch):
+    """engine.step() on a host-resident (numpy) reference-style state."""
+
+    @dataclass
+    class HostState:  # field-for-field the reference's SearchState (engine.py:376-387)
+        config: object
+        seed: int
+        population: np.ndarray
+        fitness: np.ndarray
+        iteration: int
+        best_matrix: np.ndarray
+        best_fitness: int
+        trace: list = field(default_factory=list)
+
+    dev_state = hga.initial_state(cfg)
+    pop = dev_state.population
+    fit = dev_state.fitness
+    hs = HostState(cfg, dev_state.seed, pop, fit, 0, dev_state.best_matrix, dev_state.best_fitness,
+                   [dev_state.best_fitness])
+    del dev_state
+    steps = max(3, min(args.steps, 30))
+    for _ in range(2):
+        engine.step(hs)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        engine.step(hs)
+    t = (time.perf_counter() - t0) / steps
+    assert hs.population[:, :, 0].min() == 1
+    return {"value": 2 * N_PAIRS / t, "unit": UNIT, "h2d_bytes_per_step": int(pop.nbytes + fit.nbytes + 64),
+            "d2h_bytes_per_step": int(pop.nbytes + fit.nbytes + 8), "steps": steps, "ms_per_step": t * 1e3,
+            "api": "paper_2208_14961_b200.engine.step(state) with numpy population/fitness (drop-in for "
+                   "hadamard_ga.step)"}
+
+
+def run_fitness_sweep(args, engine, torch, lib, peak):
+    sp = torch.cuda.current_stream().cuda_stream
+    rows = []
+    for m in (20, 28, 36, 64):
+        n = 4_000_000 if m <= 28 else (2_000_000 if m <= 36 else 1_000_000)
+        cfg = engine.GAConfig(order=m, population=n // 4, seed=7)
+        pop = engine.init_population_device(cfg)
+        out = torch.empty(n, dtype=torch.int64, device=pop.device)
+        fn = lambda: lib.hga_fitness_i8(pop.data_ptr(), n, m, 2, None, out.data_ptr(), None, None, None, None, 0, sp)
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            e.synchronize()
+            ts.append(s.elapsed_time(e) / 1e3)
+        t = statistics.median(ts)
+        bytes_ = n * (m * m + 8)
+        popc_ceiling = 4.52e12 / ((m * (m - 1) // 2) * ((m + 31) // 32))
+        hbm_ceiling = peak * 1e9 / (m * m + 8)
+        ev = n / t
+        rows.append({"m": m, "n": n, "evals_per_s": ev, "GBps": bytes_ / t / 1e9, "hbm_frac": bytes_ / t / 1e9 / peak,
+                     "frac_of_binding_ceiling": ev / min(popc_ceiling, hbm_ceiling),
+                     "binding": "hbm" if hbm_ceiling < popc_ceiling else "popc"})
+        del pop, out
+        torch.cuda.empty_cache()
+    return {"kernel": "hga_fitness_i8 (int8 (n,m,m) drop-in layout, F2)", "inputs": "larger than L2", "rows": rows}
+
+
+# ---------------------------------------------------------------- cpu / reference arm
+
+
+def cpu_baseline(args, budget_s: float = 12.0) -> dict:
+    import oracle
+
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    st = oracle.initial_state(ORDER, N_PAIRS, 2024, FITNESS, NC, NR, "multi", threads=threads)
+    oracle.step(st, threads)
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < budget_s and n < 400:
+        oracle.step(st, threads)
+        n += 1
+    t = time.perf_counter() - t0
+    return {"value": 2 * N_PAIRS * n / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n} generations of the same workload (order 20, 40,000 matrices, f2, NC=4, NR=2) by the C "
+                      f"oracle (oracle/hga_oracle.c, OpenMP fitness), {t:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import oracle
+
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    st = oracle.initial_state(ORDER, N_PAIRS, 2024, FITNESS, NC, NR, "multi", threads=threads)
+    for _ in range(args.warmup):
+        oracle.step(st, threads)
+    steps = args.steps
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.step(st, threads)
+    t = time.perf_counter() - t0
+    value = 2 * N_PAIRS * steps / t
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": t / steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int8 +-1 (int64 fitness)",
+        "data": "synthetic: random balanced sign matrices (reference splitmix64 streams, seed 2024)",
+        "config": {"workload": "BASELINE configs[1]: order-20 GA, population 40,000 matrices (N=10,000 pairs), "
+                               "fitness f2, mutation multi NC=4 NR=2", "order": ORDER, "matrices": 4 * N_PAIRS,
+                   "offspring_evals_per_step": 2 * N_PAIRS, "parallelism": "host threads (OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{steps} generations of the full workload by the C oracle port of the reference "
+                                   "(oracle/hga_oracle.c; the reference is pure Python/NumPy, nothing to compile)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        out = run_ours(args, rank, world, local_rank)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

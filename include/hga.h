@@ -182,7 +182,18 @@ typedef struct hga_run_args {
     uint32_t *best_matrix;    /* packed best-so-far (m * W words) */
     void *ws;                 /* hga_run_ws_bytes() */
     size_t ws_bytes;
+    uint32_t flags;           /* HGA_RUN_FORCE: run exactly gens_this_call
+                                 generations (no stop test, no restart) */
 } hga_run_args;
+
+#define HGA_RUN_FORCE 1u
+
+/* Philox balanced matrices into slots [first_slot, first_slot + count) of
+ * the packed population `cols` (slot 0 at cols).  The production-mode
+ * counterpart of hga_ref_init_packed. */
+int hga_philox_init_packed(uint64_t seed, uint64_t purpose, uint64_t generation,
+                           int64_t first_slot, int64_t count, int32_t m, uint32_t *cols,
+                           void *stream);
 
 size_t hga_run_ws_bytes(int64_t n_pairs, int32_t m);
 /* Philox-stream init of all 4N slots of pop[0] + evaluation + state init. */

@@ -230,7 +230,8 @@ __global__ void __launch_bounds__(kGenThreads) k_run(RunParams P) {
     int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
     int parity = (int)A.state[3];
     int64_t run = A.state[6], last_val = A.state[7];
-    bool stop = A.state[5] != 0;
+    const bool force = (A.flags & HGA_RUN_FORCE) != 0;
+    bool stop = !force && A.state[5] != 0;
 
     for (int64_t gi = 0; gi < A.gens_this_call && !stop; ++gi) {
         const int64_t gen = iter + 1;
@@ -434,9 +435,9 @@ __global__ void __launch_bounds__(kGenThreads) k_run(RunParams P) {
                     ws->par_key[gp ^ 1] = ~0ull;
                 }
             }
-            stop = best == 0 || iter >= A.max_generation;
+            stop = !force && (best == 0 || iter >= A.max_generation);
             // stall restart (engine.py:472-494, 518-525)
-            if (!stop && A.stall_window > 0 && iter - last_restart >= A.stall_window && run >= A.stall_window &&
+            if (!stop && !force && A.stall_window > 0 && iter - last_restart >= A.stall_window && run >= A.stall_window &&
                 last_val > 0) {
                 // refill offspring slots of the new population, evaluate them
                 uint32_t* cur = pop_new;
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(kGenThreads) k_run(RunParams P) {
         A.state[1] = best;
         A.state[2] = last_restart;
         A.state[3] = parity;
-        A.state[5] = stop ? 1 : 0;
+        A.state[5] = (best == 0 || iter >= A.max_generation) ? 1 : 0;
         A.state[6] = run;
         A.state[7] = last_val;
     }
@@ -731,6 +732,23 @@ int hga_run_init(const hga_run_args* a, void* stream) {
     if (e != cudaSuccess) return to_rc(e);
     k_argmin_key2<<<(int)std::min<int64_t>((total + 255) / 256, sm_count_cached() * 8), 256, 0, st>>>(a->fit[0], total, key);
     k_run_finish_init<<<1, 256, 0, st>>>(*a, W, key, ws);
+    return to_rc(cudaGetLastError());
+}
+
+int hga_philox_init_packed(uint64_t seed, uint64_t purpose, uint64_t generation, int64_t first_slot,
+                           int64_t count, int32_t m, uint32_t* cols, void* stream) {
+    if (count < 0 || first_slot < 0 || m < 1 || m > 32 * kMaxRegWords) return HGA_E_INVALID;
+    if (count == 0) return HGA_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t work = count * m;
+    const int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)sm_count_cached() * 16);
+    // cols points at slot 0 of the population; slots [first_slot, first_slot + count) are written
+    switch (words_for(m)) {
+        case 1: k_philox_init<1><<<grid, 256, 0, st>>>(seed, (uint32_t)purpose, generation, first_slot, count, m, cols); break;
+        case 2: k_philox_init<2><<<grid, 256, 0, st>>>(seed, (uint32_t)purpose, generation, first_slot, count, m, cols); break;
+        case 3: k_philox_init<3><<<grid, 256, 0, st>>>(seed, (uint32_t)purpose, generation, first_slot, count, m, cols); break;
+        default: k_philox_init<4><<<grid, 256, 0, st>>>(seed, (uint32_t)purpose, generation, first_slot, count, m, cols); break;
+    }
     return to_rc(cudaGetLastError());
 }
 

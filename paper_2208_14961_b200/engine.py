@@ -35,7 +35,8 @@ import torch
 
 from . import _dev
 from ._dev import HgaError, check, lib, ptr, stream_ptr, words_for
-from ._lib import FLAG_FIT_RANGE, FLAG_NOT_SIGN, FLAG_PLAN_RANGE, FLAG_POINT_RANGE, MUT_CODES, RunArgs, VARIANT_BITS
+from ._lib import (FLAG_FIT_RANGE, FLAG_NOT_SIGN, FLAG_PLAN_RANGE, FLAG_POINT_RANGE, MUT_CODES, RUN_FORCE, RunArgs,
+                   VARIANT_BITS)
 from .rand import MASK64, RngStream, random_seed
 
 __all__ = [
@@ -250,13 +251,22 @@ def _pack(pop: torch.Tensor) -> torch.Tensor:
 
 
 def init_population_device(config: GAConfig, seed: int | None = None) -> torch.Tensor:
-    """(4N, m, m) int8 CUDA tensor of the initial population (reference streams)."""
+    """(4N, m, m) int8 CUDA tensor of the initial population.
+
+    rng="reference": the reference's streams, bit-identical to
+    hadamard_ga.init_population; rng="philox": the production streams.
+    """
     if seed is None:
         seed = config.seed
     if seed is None:
         raise ValueError("init_population needs an explicit seed")
     dev = _dev.require_cuda()
     m, total = config.order, config.total
+    if config.rng == "philox" and m <= MAX_RESIDENT_ORDER:
+        packed = torch.empty(total * m * words_for(m), dtype=torch.int32, device=dev)
+        check(lib.hga_philox_init_packed(seed & MASK64, _P_INIT, 0, 0, total, m, packed.data_ptr(), stream_ptr()),
+              "hga_philox_init_packed")
+        return _unpack(packed, total, m)
     out = torch.empty((total, m, m), dtype=torch.int8, device=dev)
     if m <= MAX_RESIDENT_ORDER:
         check(lib.hga_ref_init_i8(seed & MASK64, _P_INIT, 0, 0, total, m, out.data_ptr(), stream_ptr()),
@@ -268,8 +278,8 @@ def init_population_device(config: GAConfig, seed: int | None = None) -> torch.T
 
 
 def init_population(config: GAConfig, seed: int | None = None) -> np.ndarray:
-    """Initial population of 4N balanced matrices (engine.py:185-197), bit-identical
-    to the reference's for the same seed."""
+    """Initial population of 4N balanced matrices (engine.py:185-197); with
+    rng="reference" bit-identical to the reference's for the same seed."""
     return init_population_device(config, seed).cpu().numpy()
 
 
@@ -641,26 +651,94 @@ def _run_device(state: SearchState, gens: int) -> None:
     _sync_from_device(state)
 
 
-def step(state: SearchState, workers: int = 1) -> SearchState:
-    """Advance one generation (engine.py:449-469)."""
+def step(state, workers: int = 1):
+    """Advance one generation (engine.py:449-469).
+
+    `state` is a SearchState from initial_state (device resident), or any
+    reference-style state whose population/fitness are numpy arrays (e.g.
+    hadamard_ga.SearchState): that one is copied to the GPU, advanced and
+    copied back in place, exactly like the reference's in-place step.
+    """
+    if not isinstance(state, SearchState):
+        return _step_host(state)
     if state.config.rng == "reference":
         _step_reference(state)
     else:
-        cfg = state.config
-        # one generation, ignoring the loop's own stop conditions
         res = state._res
-        res.dstate[5] = 0
-        saved = cfg.max_iterations
-        a_cap = max(saved, state.iteration + 1)
         res.ensure_trace(state.iteration + 1)
         a = res.run_args()
-        a.max_generation = a_cap
-        a.stall_window = 0
         a.gens_this_call = 1
+        a.flags = RUN_FORCE
         check(lib.hga_run(a, stream_ptr()), "hga_run")
         _sync_from_device(state)
     if DEBUG_CHECKS:
         _check_state(state)
+    return state
+
+
+class _HostBridge:
+    """Device buffers behind a host (numpy) search state; host arrays are
+    page-locked in place (cudaHostRegister) so the per-step copies are DMA."""
+
+    def __init__(self, state):
+        cfg = state.config
+        rng = getattr(cfg, "rng", "reference")
+        self.cfg = cfg if isinstance(cfg, GAConfig) else GAConfig(
+            order=cfg.order, population=cfg.population, max_iterations=cfg.max_iterations,
+            mutation_cols=cfg.mutation_cols, mutation_row_pairs=cfg.mutation_row_pairs, fitness=cfg.fitness,
+            mutation=cfg.mutation, seed=cfg.seed, stall_window=cfg.stall_window,
+            time_budget_secs=cfg.time_budget_secs, rng=rng)
+        self.res = _Resident(self.cfg, int(state.seed) & MASK64)
+        m, total = self.cfg.order, self.cfg.total
+        self.pop_i8 = torch.empty((total, m, m), dtype=torch.int8, device=self.res.dev)
+        self.registered = []
+        self.inner = SearchState(self.cfg, int(state.seed) & MASK64, self.res, 0, 0, [], None)
+
+    def pin(self, arr: np.ndarray) -> None:
+        key = (arr.ctypes.data, arr.nbytes)
+        if key in self.registered or arr.nbytes == 0:
+            return
+        rc = torch.cuda.cudart().cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+        if int(rc) == 0:
+            self.registered.append(key)
+
+
+def _step_host(state):
+    bridge = getattr(state, "_hga_bridge", None)
+    if bridge is None:
+        bridge = _HostBridge(state)
+        state._hga_bridge = bridge
+    pop_np, fit_np = state.population, state.fitness
+    if not (pop_np.flags.c_contiguous and fit_np.flags.c_contiguous):
+        raise ValueError("host population and fitness must be C-contiguous")
+    bridge.pin(pop_np)
+    bridge.pin(fit_np)
+    res, inner = bridge.res, bridge.inner
+    res.cur = cur = 0  # the host arrays are authoritative: upload into buffer 0
+    bridge.pop_i8.copy_(torch.from_numpy(pop_np), non_blocking=True)
+    res.fit[cur].copy_(torch.from_numpy(fit_np), non_blocking=True)
+    flag = _dev.new_flag()
+    m, total = res.m, 4 * res.N
+    check(lib.hga_pack_i8(bridge.pop_i8.data_ptr(), total, m, res.pop[cur].data_ptr(), flag.data_ptr(),
+                          stream_ptr()), "hga_pack_i8")
+    inner.iteration, inner.best_fitness = int(state.iteration), int(state.best_fitness)
+    inner.trace = [int(state.trace[-1])] if state.trace else [int(state.best_fitness)]
+    res.dstate.copy_(torch.tensor([inner.iteration, inner.best_fitness, 0, cur, 0, 0, 1, inner.trace[-1]],
+                                  dtype=torch.int64), non_blocking=True)
+    inner.best_matrix = None
+    step(inner)
+    check(lib.hga_unpack_i8(res.pop[res.cur].data_ptr(), total, m, bridge.pop_i8.data_ptr(), stream_ptr()),
+          "hga_unpack_i8")
+    torch.from_numpy(pop_np).copy_(bridge.pop_i8, non_blocking=True)
+    torch.from_numpy(fit_np).copy_(res.fit[res.cur], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    _check_flag(flag, "step")
+    fmin = inner.trace[-1]
+    state.iteration = inner.iteration
+    state.trace.append(fmin)
+    if fmin < state.best_fitness:
+        state.best_fitness = fmin
+        state.best_matrix = pop_np[int(np.argmin(fit_np))].copy()
     return state
 
 

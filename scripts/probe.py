@@ -55,7 +55,7 @@ def probe_fitness(quick):
         n = 2_000_000 if m <= 32 else (1_000_000 if m <= 64 else 200_000)
         if quick:
             n //= 4
-        cfg = engine.GAConfig(order=m, population=n // 4, seed=2024, rng="reference")
+        cfg = engine.GAConfig(order=m, population=n // 4, seed=2024)
         pop = engine.init_population_device(cfg)
         outs = torch.empty(n, dtype=torch.int64, device="cuda")
         for var, name in ((2, "f2"), (1, "f1"), (15, "all")):
