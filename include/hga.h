@@ -183,10 +183,12 @@ typedef struct hga_run_args {
     void *ws;                 /* hga_run_ws_bytes() */
     size_t ws_bytes;
     uint32_t flags;           /* HGA_RUN_FORCE: run exactly gens_this_call
-                                 generations (no stop test, no restart) */
+                                 generations (no stop test, no restart);
+                                 HGA_RUN_TIMING: phase timestamps */
 } hga_run_args;
 
 #define HGA_RUN_FORCE 1u
+#define HGA_RUN_TIMING 2u  /* record per-phase %globaltimer stamps (diagnostics) */
 
 /* Philox balanced matrices into slots [first_slot, first_slot + count) of
  * the packed population `cols` (slot 0 at cols).  The production-mode
@@ -196,8 +198,15 @@ int hga_philox_init_packed(uint64_t seed, uint64_t purpose, uint64_t generation,
                            void *stream);
 
 size_t hga_run_ws_bytes(int64_t n_pairs, int32_t m);
+/* byte offset inside ws of the uint64 [64][12] phase timestamps (HGA_RUN_TIMING),
+ * or -1 when the order runs on the fallback loop */
+int64_t hga_run_timing_offset(int32_t m);
 /* Philox-stream init of all 4N slots of pop[0] + evaluation + state init. */
 int hga_run_init(const hga_run_args *args, void *stream);
+/* Rebuild the loop's selection state (histogram, keys) from the current
+ * population pop/fit[state[3]]; call after replacing the population or the
+ * state block from outside (hga_run_init already does it). */
+int hga_run_prepare(const hga_run_args *args, void *stream);
 int hga_run(const hga_run_args *args, void *stream);
 
 #ifdef __cplusplus

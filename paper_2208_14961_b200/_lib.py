@@ -27,6 +27,7 @@ VARIANT_BITS = {"f1": VAR_F1, "f2": VAR_F2, "orth": VAR_ORTH, "sq": VAR_SQ}
 FLAG_NOT_SIGN, FLAG_POINT_RANGE, FLAG_PLAN_RANGE, FLAG_FIT_RANGE = 1, 2, 4, 8
 
 RUN_FORCE = 1
+RUN_TIMING = 2
 
 MUT_CODES = {"shared": 0, "per-matrix": 1, "multi": 2}
 
@@ -92,7 +93,9 @@ SIGNATURES = {
     "hga_argmin_key": (_int, [_vp, _i64, _vp, _int, _vp]),
     "hga_philox_init_packed": (_int, [_u64, _u64, _u64, _i64, _i64, _i32, _vp, _vp]),
     "hga_run_ws_bytes": (_sz, [_i64, _i32]),
+    "hga_run_timing_offset": (_i64, [_i32]),
     "hga_run_init": (_int, [ctypes.POINTER(RunArgs), _vp]),
+    "hga_run_prepare": (_int, [ctypes.POINTER(RunArgs), _vp]),
     "hga_run": (_int, [ctypes.POINTER(RunArgs), _vp]),
 }
 

@@ -12,9 +12,22 @@
 // columns stored twice (so i + d never wraps).  For the int8 input the CTA
 // first stages mpb * m * m bytes with 16-byte loads (validating every byte is
 // +-1 on the way), then each thread packs its own column from shared memory.
-#include "hga_common.cuh"
+#include "fitness_v2.cuh"
 
 namespace hga {
+
+HGA_V2_ORDERS(HGA_V2_EXTERN)
+
+static int launch_fit_v2(int m, bool from_i8, const void* src, int64_t n, uint32_t v, int64_t* f1, int64_t* f2,
+                         int64_t* orth, int64_t* sq, int32_t* bad, cudaStream_t st) {
+    switch (m) {
+#define HGA_V2_CASE(M) \
+    case M: return launch_fit_v2_m<M>(from_i8, src, n, v, f1, f2, orth, sq, bad, st);
+        HGA_V2_ORDERS(HGA_V2_CASE)
+#undef HGA_V2_CASE
+        default: return HGA_E_UNSUPPORTED;
+    }
+}
 
 constexpr int kFitThreads = 256;
 
@@ -310,6 +323,8 @@ int hga_fitness_i8(const int8_t* pop, int64_t n, int32_t m, uint32_t variants, i
     if (n < 0 || m < 1 || m > 4096 || (variants & ~HGA_VAR_ALL) || !variants) return HGA_E_INVALID;
     if (n == 0) return HGA_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (v2_order(m) && (((uintptr_t)pop) & 15) == 0)
+        return launch_fit_v2(m, true, pop, n, variants, f1, f2, orth, sq, bad_flag, st);
     if (m <= 32 * kMaxRegWords)
         return launch_fitness<true>(pop, n, m, variants, f1, f2, orth, sq, bad_flag, st);
     const int W = words_for(m);
@@ -330,6 +345,8 @@ int hga_fitness_packed(const uint32_t* cols, int64_t n, int32_t m, uint32_t vari
     if (n < 0 || m < 1 || m > 4096 || (variants & ~HGA_VAR_ALL) || !variants) return HGA_E_INVALID;
     if (n == 0) return HGA_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (v2_order(m) && (((uintptr_t)cols) & 15) == 0)
+        return launch_fit_v2(m, false, cols, n, variants, f1, f2, orth, sq, nullptr, st);
     if (m <= 32 * kMaxRegWords)
         return launch_fitness<false>(cols, n, m, variants, f1, f2, orth, sq, nullptr, st);
     k_fitness_any<<<(unsigned)std::min<int64_t>(n, sm_count_cached() * 8), 128, 0, st>>>(

@@ -19,6 +19,10 @@
 //      F  trace / best / stop / stall-restart bookkeeping, replicated in every
 //         CTA from the same global values so all CTAs agree without a barrier
 #include "generation.cuh"
+#include "run_common.cuh"
+#include "run_v2.cuh"
+
+#include <cstddef>
 
 namespace hga {
 
@@ -53,87 +57,6 @@ __global__ void __launch_bounds__(kGenThreads)
         __syncthreads();
         offspring_tile<W, VM, false>(s, pop, pop, fit, N, p0, cnt, ppb, m, nc, nr, fit_var, best_key);
     }
-}
-
-// ======================================================== Philox helpers
-__device__ __forceinline__ U4 draw4(uint64_t seed, uint32_t a, uint32_t b, uint64_t gen, uint32_t purpose) {
-    return philox(U4{a, b, (uint32_t)gen, (purpose << 24) ^ (uint32_t)(gen >> 32)}, (uint32_t)seed,
-                  (uint32_t)(seed >> 32));
-}
-__device__ __forceinline__ uint32_t pick(const U4& v, int i) {
-    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-}
-
-__device__ __forceinline__ uint32_t hash32(uint32_t x) {
-    x ^= x >> 16;
-    x *= 0x7FEB352Du;
-    x ^= x >> 15;
-    x *= 0x846CA68Bu;
-    x ^= x >> 16;
-    return x;
-}
-
-// Keyed bijection on [0, n) (4-round balanced Feistel + cycle walking).
-__device__ __forceinline__ uint32_t feistel(uint32_t x, uint32_t n, int hb, const U4& k) {
-    const uint32_t mask = (1u << hb) - 1u;
-    do {
-        uint32_t L = x >> hb, R = x & mask;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const uint32_t f = hash32(R ^ pick(k, r)) & mask;
-            const uint32_t nl = R;
-            R = L ^ f;
-            L = nl;
-        }
-        x = (L << hb) | R;
-    } while (x >= n);
-    return x;
-}
-
-// Philox balanced column (Fisher-Yates over the m rows with Lemire draws).
-template <int W>
-__device__ __forceinline__ void philox_column(uint64_t seed, uint32_t purpose, uint64_t gen, int64_t slot,
-                                              int m, int c, Col<W>& col) {
-#pragma unroll
-    for (int w = 0; w < W; ++w) col.w[w] = 0;
-    if (c == 0) return;
-    const int h = m / 2;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-        const int lo = 32 * w, hi = min(32 * w + 32, h);
-        if (hi > lo) col.w[w] = (hi - lo == 32) ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u);
-    }
-    U4 r{0, 0, 0, 0};
-    for (int a = 0; a + 1 < m; ++a) {
-        if ((a & 3) == 0)
-            r = draw4(seed, (uint32_t)slot, (uint32_t)c | ((uint32_t)(a >> 2) << 12) | ((uint32_t)(slot >> 32) << 24), gen, purpose);
-        const int b = a + (int)bounded(pick(r, a & 3), (uint32_t)(m - a));
-        swap_rows<W>(col, a, b);
-    }
-}
-
-// ======================================================== grid barrier
-struct Barrier {
-    unsigned int count;
-    unsigned int gen;
-};
-
-__device__ __forceinline__ void grid_sync(Barrier* b) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned int* vg = &b->gen;
-        const unsigned int g = *vg;
-        __threadfence();
-        if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
-            b->count = 0;
-            __threadfence();
-            atomicExch(&b->gen, g + 1);
-        } else {
-            while (*vg == g) __nanosleep(20);
-        }
-        __threadfence();
-    }
-    __syncthreads();
 }
 
 // ======================================================== run workspace
@@ -669,6 +592,65 @@ static int launch_explicit_w(uint32_t* pop, int64_t* fit, int64_t N, int m, cons
     }
 }
 
+HGA_R2_ORDERS(HGA_R2_EXTERN)
+
+int run2_granule_shift(uint32_t fit_var) { return fit_var == HGA_VAR_F1 ? 3 : (fit_var == HGA_VAR_SQ ? 5 : 1); }
+
+bool run2_supported(const hga_run_args* a) {
+    const int m = a->m;
+    if (m < 4 || m > 64 || (m & 3)) return false;
+    if (a->fit_var == HGA_VAR_SQ && m > 32) return false;
+    const int nc = a->strategy == HGA_MUT_MULTI ? a->nc : 1, nr = a->strategy == HGA_MUT_MULTI ? a->nr : 1;
+    if (nc + 2 * nr > kR2MaxPlan) return false;
+    return (max_fitness(m, a->fit_var) >> run2_granule_shift(a->fit_var)) < (uint64_t)kR2Bins;
+}
+
+static int launch_run_v2(const hga_run_args* a, cudaStream_t st) {
+    switch (a->m) {
+#define HGA_R2_CASE(M) \
+    case M: return launch_run_v2_m<M>(a, st);
+        HGA_R2_ORDERS(HGA_R2_CASE)
+#undef HGA_R2_CASE
+        default: return HGA_E_UNSUPPORTED;
+    }
+}
+
+// Rebuild the select histogram of pop/fit[parity] (state[3]) and reset keys:
+// needed after init and whenever the population was replaced from outside.
+__global__ void k_run2_prepare_zero(RunWs2* ws) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < 2 * kR2Bins; b += gridDim.x * blockDim.x)
+        (&ws->hist[0][0])[b] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ws->bar.count = 0;
+        ws->bar.gen = 0;
+        ws->best_key[0] = ws->best_key[1] = ~0ull;
+        ws->par_key[0] = ws->par_key[1] = ~0ull;
+        ws->restart_key = ~0ull;
+        ws->kmin[0] = ws->kmin[1] = 0xffffffffu;
+        ws->kmax[0] = ws->kmax[1] = 0u;
+    }
+}
+
+__global__ void k_run2_prepare_hist_state(RunWs2* ws, hga_run_args a, int gshift) {
+    const int slot = (int)((a.state[0] + 1) & 1);
+    const int64_t* fit = a.fit[a.state[3]];
+    const int64_t total = 4 * a.n_pairs;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < total; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool ok = i < total;
+        hist_add(ws, slot, ok, ok ? (uint32_t)(fit[i] >> gshift) : 0u);
+    }
+}
+
+static int run2_prepare(const hga_run_args* a, cudaStream_t st) {
+    RunWs2* ws = (RunWs2*)a->ws;
+    const int64_t total = 4 * a->n_pairs;
+    k_run2_prepare_zero<<<64, 256, 0, st>>>(ws);
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count_cached() * 8);
+    k_run2_prepare_hist_state<<<std::max(grid, 1), 256, 0, st>>>(ws, *a, run2_granule_shift(a->fit_var));
+    return to_rc(cudaGetLastError());
+}
+
 }  // namespace hga
 
 using namespace hga;
@@ -695,8 +677,9 @@ int hga_generation_explicit(uint32_t* pop, int64_t* fit, int64_t n_pairs, int32_
 
 size_t hga_run_ws_bytes(int64_t n_pairs, int32_t m) {
     (void)m;
-    return run_ws_head() + (size_t)(2 * n_pairs) * 8;
+    return std::max(run_ws_head() + (size_t)(2 * n_pairs) * 8, run_ws2_head() + (size_t)(8 * n_pairs) * 4);
 }
+
 
 static int run_args_ok(const hga_run_args* a) {
     if (!a || a->n_pairs < 1 || a->m < 4 || a->m > 32 * kMaxRegWords || (a->m & 3) || !valid_var(a->fit_var))
@@ -707,6 +690,25 @@ static int run_args_ok(const hga_run_args* a) {
     if (!a->pop[0] || !a->pop[1] || !a->fit[0] || !a->fit[1] || !a->state || !a->best_matrix || !a->ws) return 0;
     if (a->ws_bytes < hga_run_ws_bytes(a->n_pairs, a->m)) return 0;
     return 1;
+}
+
+int64_t hga_run_timing_offset(int32_t m) {
+    if (m < 4 || m > 64 || (m & 3)) return -1;
+    return (int64_t)offsetof(RunWs2, tstamp);
+}
+
+int hga_run_prepare(const hga_run_args* a, void* stream) {
+    if (!run_args_ok(a)) return HGA_E_INVALID;
+    if (!run2_supported(a)) {
+        // v1 keeps no cross-generation histogram; only the keys need a reset
+        RunWs* ws = (RunWs*)a->ws;
+        cudaStream_t st = (cudaStream_t)stream;
+        cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(Barrier), st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(&ws->best_key[0], 0xFF, 5 * sizeof(unsigned long long), st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(&ws->hist1[0], 0, 2 * kHistBins * sizeof(uint32_t), st);
+        return to_rc(e);
+    }
+    return run2_prepare(a, (cudaStream_t)stream);
 }
 
 int hga_run_init(const hga_run_args* a, void* stream) {
@@ -732,7 +734,10 @@ int hga_run_init(const hga_run_args* a, void* stream) {
     if (e != cudaSuccess) return to_rc(e);
     k_argmin_key2<<<(int)std::min<int64_t>((total + 255) / 256, sm_count_cached() * 8), 256, 0, st>>>(a->fit[0], total, key);
     k_run_finish_init<<<1, 256, 0, st>>>(*a, W, key, ws);
-    return to_rc(cudaGetLastError());
+    rc = to_rc(cudaGetLastError());
+    if (rc) return rc;
+    if (run2_supported(a)) return run2_prepare(a, st);
+    return HGA_OK;
 }
 
 int hga_philox_init_packed(uint64_t seed, uint64_t purpose, uint64_t generation, int64_t first_slot,
@@ -756,6 +761,7 @@ int hga_run(const hga_run_args* a, void* stream) {
     if (!run_args_ok(a)) return HGA_E_INVALID;
     if (a->gens_this_call <= 0) return HGA_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (run2_supported(a)) return launch_run_v2(a, st);
     switch (words_for(a->m)) {
         case 1: return launch_run_w<1>(a, st);
         case 2: return launch_run_w<2>(a, st);

@@ -1,0 +1,857 @@
+// run_v2.cuh -- the production generation loop for GA orders m = 4..64
+// (step / run_search, reference engine.py:449-538, with Philox streams).
+//
+// One persistent cooperative kernel runs a batch of generations; each
+// generation is three grid-barrier-separated phases:
+//   B  every CTA reads the select histogram of the current population (built
+//      during the previous generation, keys = fitness >> granule, exact
+//      because every balanced GA matrix has F1 = 0 mod 8, F2 = 0 mod 2,
+//      SQ = 0 mod 32), finds the threshold tau and the tie quota for the 2N
+//      survivors (lowest index first on ties, engine.py:245), and counts
+//      (F < tau, F == tau) over its contiguous index range
+//   D  survivor ranks (CTA prefix + block scan, index order) -> parent slot
+//      through a keyed Feistel bijection (uniformly random placement,
+//      engine.py:246); survivors' keys go into the NEXT generation's
+//      histogram
+//   E  offspring tiles, one thread per offspring: the CTA gathers the 64
+//      pairs' parents into shared memory (and writes them to the new
+//      population's parent slots), each thread assembles its child's columns
+//      (column-block crossover, engine.py:257-277), applies its Philox
+//      mutation plan to them in shared memory (engine.py:339-373), loads the
+//      M column words into registers and runs the unrolled XOR+POPC pair
+//      chain (column 0 is all +1 in every GA individual, so its pairs are 0)
+//   F  bookkeeping replicated in every CTA (trace, best, stop, stall restart)
+#pragma once
+
+#include "run_common.cuh"
+#include "tile.cuh"
+
+namespace hga {
+
+constexpr int kR2Threads = 128;
+constexpr int kTeam = 4;                          // threads (warps) per offspring in the pair chain
+constexpr int kTileOff = kR2Threads / kTeam;      // 32 offspring per tile
+constexpr int kR2Pairs = kTileOff / 2;            // 16 parent pairs per tile
+constexpr int kSelItems = 8;                      // fitness values per thread in the select scans
+constexpr int kR2Bins = 32768;
+constexpr int kR2MaxGrid = 2048;
+constexpr int kR2MaxPlan = 128;  // nc + 2 nr <= (m - 1) + m
+
+struct RunWs2 {
+    Barrier bar;
+    unsigned long long best_key[2];
+    unsigned long long par_key[2];
+    unsigned long long restart_key;
+    uint32_t kmin[2];
+    uint32_t kmax[2];
+    uint32_t cnt_lt[kR2MaxGrid];
+    uint32_t cnt_eq[kR2MaxGrid];
+    uint32_t hist[2][kR2Bins];
+    unsigned long long tstamp[64][12];  // HGA_RUN_TIMING: %globaltimer at phase boundaries (CTA 0)
+    // followed by lt_list[4N], eq_list[4N] (int32): each CTA's survivors, compacted in index order
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__host__ __device__ inline size_t run_ws2_head() { return (sizeof(RunWs2) + 255) & ~(size_t)255; }
+
+template <int M>
+struct RunGeom {
+    static constexpr int W = Order<M>::W;
+    static constexpr int MW = M * W;
+    static constexpr int U = MW / 4;                      // 16B units per matrix (M multiple of 4)
+    static constexpr int STU = (U & 1) ? U : U + 1;       // odd stride: conflict-free per-thread LDS.128
+    static constexpr int ROWS = kTileOff * STU * 16;      // parent rows, turned into the children in place
+    static constexpr int SMEM = ROWS;
+    static constexpr int NP = (M - 1) * (M - 2) / 2;      // pairs with column 0 skipped
+};
+
+// ------------------------------------------------------------ helpers
+__device__ __forceinline__ void group_sync(int g) {
+    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kR2Threads) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t* p) { return __ldcg(p); }
+
+// Block-wide: first bin b (in [0, bins)) where the inclusive prefix of h
+// reaches k; also the count strictly below b.  h is read with ld.cg.
+__device__ inline void kth_bin_cg(const uint32_t* h, int bins, uint64_t k, int* out_bin, uint64_t* out_below,
+                           uint64_t* scratch) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int per = (bins + nt - 1) / nt;
+    const int b0 = tid * per;
+    uint64_t mine = 0;
+    for (int b = b0; b < min(bins, b0 + per); ++b) mine += ld_cg_u32(h + b);
+    uint64_t x = mine;
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) scratch[wid] = x;
+    __syncthreads();
+    if (tid == 0) {
+        uint64_t run = 0;
+        for (int w = 0; w < nt / 32; ++w) {
+            const uint64_t t = scratch[w];
+            scratch[w] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+    const uint64_t excl = scratch[wid] + x - mine;
+    if (excl < k && excl + mine >= k) {
+        uint64_t run = excl;
+        for (int b = b0; b < min(bins, b0 + per); ++b) {
+            const uint32_t hb = ld_cg_u32(h + b);
+            if (run + hb >= k) {
+                *out_bin = b;
+                *out_below = run;
+                break;
+            }
+            run += hb;
+        }
+    }
+    __syncthreads();
+}
+
+// One warp: first bin b (in [0, bins)) where the inclusive prefix of h
+// reaches k (1 <= k <= total), and the count strictly below b.
+__device__ inline void kth_bin_warp(const uint32_t* h, int bins, uint64_t k, int* out_bin, uint64_t* out_below) {
+    const int lane = threadIdx.x & 31;
+    uint64_t run = 0;
+    for (int b0 = 0; b0 < bins; b0 += 32) {
+        const int b = b0 + lane;
+        const uint32_t v = b < bins ? __ldcg(h + b) : 0u;
+        uint64_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const bool hit = (run + x >= k) && (run + x - v < k);
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (m) {
+            if (lane == __ffs(m) - 1) {
+                *out_bin = b;
+                *out_below = run + x - v;
+            }
+            return;
+        }
+        run += __shfl_sync(0xffffffffu, x, 31);
+    }
+}
+
+// Warp-aggregated histogram + key-range update for the next generation.
+__device__ __forceinline__ void hist_add(RunWs2* ws, int slot, bool valid, uint32_t key) {
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!act) return;
+    const unsigned peers = __match_any_sync(0xffffffffu, valid ? key : 0xffffffffu);
+    if (valid && (__ffs(peers & act) - 1) == (int)(threadIdx.x & 31))
+        atomicAdd(&ws->hist[slot][key], (uint32_t)__popc(peers & act));
+    uint32_t mn = valid ? key : 0xffffffffu, mx = valid ? key : 0u;
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&ws->kmin[slot], mn);
+        atomicMax(&ws->kmax[slot], mx);
+    }
+}
+
+// Per-CTA accumulation of the next generation's histogram (shared-memory
+// window around the current minimum key, global atomics outside it), key
+// range and best keys; flushed once per CTA per phase instead of one global
+// atomic per warp on a handful of hot addresses.
+constexpr int kWin = 1024;
+
+struct LocalAcc {
+    uint32_t* s_hist;   // [kWin]
+    uint32_t wbase;     // key of s_hist[0]
+    uint32_t kmin, kmax;
+    unsigned long long best;   // min (F << 32 | slot) over this thread's parents + children
+    unsigned long long pbest;  // same over parents only
+};
+
+__device__ __forceinline__ void local_hist_add(LocalAcc& L, RunWs2* ws, int slot, bool valid, uint32_t key) {
+    if (valid) {
+        L.kmin = min(L.kmin, key);
+        L.kmax = max(L.kmax, key);
+    }
+    const uint32_t rel = key - L.wbase;
+    const bool in_win = valid && rel < (uint32_t)kWin;
+    const unsigned peers = __match_any_sync(0xffffffffu, valid ? key : 0xffffffffu);
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (valid && (__ffs(peers & act) - 1) == (int)(threadIdx.x & 31)) {
+        if (in_win) atomicAdd(&L.s_hist[rel], (uint32_t)__popc(peers & act));
+        else atomicAdd(&ws->hist[slot][key], (uint32_t)__popc(peers & act));
+    }
+}
+
+__device__ __forceinline__ void key_min_warp(unsigned long long* dst, unsigned long long k) {
+    for (int o = 16; o; o >>= 1) k = min(k, __shfl_xor_sync(0xffffffffu, k, o));
+    if ((threadIdx.x & 31) == 0 && k != ~0ull) atomicMin(dst, k);
+}
+
+// kSelItems consecutive fitness values (16-byte loads; i0 is a multiple of
+// kSelItems, so aligned), zero past `hi`.
+__device__ __forceinline__ void load_items(const int64_t* f, int64_t i0, int64_t hi, int64_t (&out)[kSelItems]) {
+    if (i0 + kSelItems <= hi) {
+#pragma unroll
+        for (int u = 0; u < kSelItems / 2; ++u) {
+            const longlong2 v = __ldcg(reinterpret_cast<const longlong2*>(f + i0) + u);
+            out[2 * u] = v.x;
+            out[2 * u + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < kSelItems; ++u) out[u] = (i0 + u < hi) ? __ldcg(f + i0 + u) : 0;
+    }
+}
+
+// Keyed bijection on [0, n): six alternating xor-rounds on a (bl | br)-bit
+// split of the smallest power-of-two domain >= n, plus cycle walking
+// (domain < 2n, so fewer than two walks on average).
+struct FeistelKey {
+    uint32_t k[6];
+    uint32_t n;
+    int bl, br;
+};
+
+__device__ __forceinline__ FeistelKey make_feistel_key(const U4& r, uint32_t n) {
+    FeistelKey f;
+    f.k[0] = r.x;
+    f.k[1] = r.y;
+    f.k[2] = r.z;
+    f.k[3] = r.w;
+    f.k[4] = hash32(r.x ^ 0x68E31DA4u);
+    f.k[5] = hash32(r.y ^ 0xB5297A4Du);
+    f.n = n;
+    int b = 0;
+    for (uint32_t x = n > 1 ? n - 1 : 1; x; x >>= 1) ++b;
+    b = b < 2 ? 2 : b;
+    f.bl = b / 2;
+    f.br = b - b / 2;
+    return f;
+}
+
+__device__ __forceinline__ uint32_t feistel2_inv(uint32_t y, const FeistelKey& f) {
+    const uint32_t ml = (1u << f.bl) - 1u, mr = (1u << f.br) - 1u;
+    do {
+        uint32_t L = y >> f.br, R = y & mr;
+#pragma unroll
+        for (int r = 4; r >= 0; r -= 2) {
+            R ^= hash32(L ^ f.k[r + 1]) & mr;
+            L ^= hash32(R ^ f.k[r]) & ml;
+        }
+        y = (L << f.br) | R;
+    } while (y >= f.n);
+    return y;
+}
+
+__device__ __forceinline__ uint32_t feistel2(uint32_t x, const FeistelKey& f) {
+    const uint32_t ml = (1u << f.bl) - 1u, mr = (1u << f.br) - 1u;
+    do {
+        uint32_t L = x >> f.br, R = x & mr;
+#pragma unroll
+        for (int r = 0; r < 6; r += 2) {
+            L ^= hash32(R ^ f.k[r]) & ml;
+            R ^= hash32(L ^ f.k[r + 1]) & mr;
+        }
+        x = (L << f.br) | R;
+    } while (x >= f.n);
+    return x;
+}
+
+struct Run2Params {
+    hga_run_args a;
+    int gshift;  // granule shift of the selection keys
+};
+
+template <int M, int VM, int F, int B0, int... Ps>
+__device__ __forceinline__ void pair_seq_at(const uint32_t (&c)[M * Order<M>::W], Sums& s,
+                                            std::integer_sequence<int, Ps...>) {
+    (pair_one<M, VM, pair_i(M, F, B0 + Ps), pair_j(M, F, B0 + Ps)>(c, s), ...);
+}
+
+// Team member K's quarter of the pair list (column 0 skipped).
+template <int M, int VM, int K>
+__device__ __forceinline__ void pair_part(const uint32_t (&c)[M * Order<M>::W], Sums& s) {
+    constexpr int NP = RunGeom<M>::NP;
+    constexpr int B0 = NP * K / kTeam, B1 = NP * (K + 1) / kTeam;
+    pair_seq_at<M, VM, 1, B0>(c, s, std::make_integer_sequence<int, B1 - B0>{});
+}
+
+constexpr int kPlanStride = kR2MaxPlan + 4;  // 33 words: plan rows of 32 children hit 32 banks
+
+struct TileShared {  // one per 128-thread tile group
+    int16_t point[kR2Pairs];
+    int32_t pidx[2 * kR2Pairs];  // old-population index of parent row 2q (A) / 2q+1 (B)
+    int8_t plan[kTileOff][kPlanStride];
+    uint32_t part[kTeam][4][kTileOff];  // child-minor: conflict-free
+};
+
+// Survivor lists: CTA b's lt survivors (F < tau) and eq candidates (F == tau)
+// are compacted in index order at [b * chunk, ...); rank order is all lt
+// survivors (CTA-major), then the first `quota` eq candidates.  Any fixed
+// bijection works here because the Feistel permutation randomises the slots.
+struct SelView {
+    const uint32_t* lt_pre;  // [nb + 1] exclusive prefix, in shared memory
+    const uint32_t* eq_pre;
+    int nb;
+    int64_t chunk;
+    const int32_t* lt_list;
+    const int32_t* eq_list;
+    uint32_t total_lt;
+};
+
+__device__ __forceinline__ int upper_bound_u32(const uint32_t* a, int n, uint32_t v) {
+    int lo = 0, hi = n;  // first index with a[i] > v
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int32_t survivor_by_rank(const SelView& V, uint32_t r) {
+    if (r < V.total_lt) {
+        const int b = upper_bound_u32(V.lt_pre, V.nb + 1, r) - 1;
+        return __ldcg(V.lt_list + (int64_t)b * V.chunk + (r - V.lt_pre[b]));
+    }
+    const uint32_t e = r - V.total_lt;
+    const int b = upper_bound_u32(V.eq_pre, V.nb + 1, e) - 1;
+    return __ldcg(V.eq_list + (int64_t)b * V.chunk + (e - V.eq_pre[b]));
+}
+
+// Offspring tile of one 128-thread group: pairs [p0, p0 + cnt), cnt <= 16.
+// Parent slot s (p for A, N + p for B) holds the survivor of rank
+// Feistel^-1(s); its row is gathered, copied to slot s of the new population,
+// and -- rows 2q / 2q+1 -- turned into O1 / O2 in place by swapping the
+// columns j >= point (engine.py:257-277).  Children are mutated by column
+// (warp k owns the columns = k mod 4, engine.py:339-373), then each warp runs
+// a quarter of the pair chain of all children.
+template <int M, int VM>
+__device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2* ws, const SelView& V,
+                                                  const FeistelKey& fkey, const uint32_t* __restrict__ pop_old,
+                                                  uint32_t* __restrict__ pop_new, const int64_t* __restrict__ f_old,
+                                                  int64_t* __restrict__ f_new, int64_t p0, int cnt, int nc, int nr,
+                                                  uint64_t gen, int gp, int gshift, uint4* rows, TileShared& S,
+                                                  LocalAcc& L, int g) {
+    using G = RunGeom<M>;
+    constexpr int W = G::W;
+    const int64_t N = A.n_pairs;
+    const int t = threadIdx.x & (kR2Threads - 1), k = t >> 5, o = t & 31;
+    const int noff = 2 * cnt;
+    const int per_off = nc + 2 * nr;
+    const int nblk = (per_off + 3) >> 2;
+
+    // a. crossover points, parents (select: slot -> rank -> survivor), Philox plans
+    if (t < cnt) {
+        const int64_t p = p0 + t;
+        const U4 r = draw4(A.seed, (uint32_t)p, (uint32_t)(p >> 32), gen, (uint32_t)kPCrossover);
+        S.point[t] = (int16_t)(1 + bounded(r.x, (uint32_t)(M - 1)));
+    }
+    if (k == 0) {
+        const bool act = o < noff;
+        int64_t f = 0;
+        if (act) {
+            const int q = o >> 1, b = o & 1;
+            const int64_t slot = (int64_t)b * N + p0 + q;
+            const int32_t idx = survivor_by_rank(V, feistel2_inv((uint32_t)slot, fkey));
+            S.pidx[o] = idx;
+            f = __ldcg(f_old + idx);
+            f_new[slot] = f;
+            const unsigned long long key = ((unsigned long long)f << 32) | (unsigned long long)slot;
+            L.best = min(L.best, key);
+            L.pbest = min(L.pbest, key);
+        }
+        local_hist_add(L, ws, gp ^ 1, act, (uint32_t)(f >> gshift));
+    }
+    for (int x = t; x < noff * nblk; x += kR2Threads) {
+        const int ol = x / nblk, blk = x - (x / nblk) * nblk;
+        const int q = ol >> 1;
+        int64_t prow = (ol & 1) ? N + p0 + q : p0 + q;  // plan row as engine.py: O1 -> p, O2 -> N + p
+        if (A.strategy == HGA_MUT_SHARED) prow = 0;
+        const U4 r = draw4(A.seed, (uint32_t)prow, (uint32_t)blk | ((uint32_t)(prow >> 32) << 16), gen,
+                           (uint32_t)kPMutCol);
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+            const int e = blk * 4 + e4;
+            if (e < per_off)
+                S.plan[ol][e] = (int8_t)(e < nc ? 1 + bounded(pick(r, e4), (uint32_t)(M - 1))
+                                                : bounded(pick(r, e4), (uint32_t)M));
+        }
+    }
+    group_sync(g);
+    // b. gather the parents; write them to the new population's parent slots
+    for (int x = t; x < noff * G::U; x += kR2Threads) {
+        const int b = x / (cnt * G::U);
+        const int r = x - b * cnt * G::U;
+        const int q = r / G::U, u = r - q * G::U;
+        const int pi = 2 * q + b;
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(pop_old + (int64_t)S.pidx[pi] * G::MW) + u);
+        rows[pi * G::STU + u] = v;
+        reinterpret_cast<uint4*>(pop_new + ((int64_t)b * N + p0 + q) * G::MW)[u] = v;
+    }
+    group_sync(g);
+    // c. column-block crossover in place
+    for (int x = t; x < cnt * M; x += kR2Threads) {
+        const int q = x / M, j = x - q * M;
+        if (j >= S.point[q]) {
+            uint32_t* ra = reinterpret_cast<uint32_t*>(rows + (2 * q) * G::STU) + j * W;
+            uint32_t* rb = reinterpret_cast<uint32_t*>(rows + (2 * q + 1) * G::STU) + j * W;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const uint32_t tmp = ra[w];
+                ra[w] = rb[w];
+                rb[w] = tmp;
+            }
+        }
+    }
+    group_sync(g);
+    // d. mutation: warp k applies, in plan order, the entries whose column is k mod 4
+    if (o < noff) {
+        uint32_t* row = reinterpret_cast<uint32_t*>(rows + o * G::STU);
+        const int8_t* pl = S.plan[o];
+        for (int jc = 0; jc < nc; ++jc) {
+            const int col = pl[jc];
+            if ((col & (kTeam - 1)) != k) continue;
+            uint32_t* cw = row + col * W;
+            for (int ir = 0; ir < nr; ++ir) {
+                const int ra = pl[nc + ir], rb = pl[nc + nr + ir];
+                uint32_t* wa = cw + (ra >> 5);
+                uint32_t* wb = cw + (rb >> 5);
+                const uint32_t xa = (*wa >> (ra & 31)) & 1u, xb = (*wb >> (rb & 31)) & 1u;
+                if (xa != xb) {
+                    *wa ^= 1u << (ra & 31);
+                    *wb ^= 1u << (rb & 31);
+                }
+            }
+        }
+    }
+    group_sync(g);
+    // e. pair chain, a quarter per warp
+    if (o < noff) {
+        uint32_t c[G::MW];
+#pragma unroll
+        for (int u = 0; u < G::U; ++u) {
+            const uint4 v = rows[o * G::STU + u];
+            c[4 * u] = v.x;
+            c[4 * u + 1] = v.y;
+            c[4 * u + 2] = v.z;
+            c[4 * u + 3] = v.w;
+        }
+        Sums s{0, 0, 0, 0};
+        switch (k) {
+            case 0: pair_part<M, VM, 0>(c, s); break;
+            case 1: pair_part<M, VM, 1>(c, s); break;
+            case 2: pair_part<M, VM, 2>(c, s); break;
+            default: pair_part<M, VM, 3>(c, s); break;
+        }
+        S.part[k][0][o] = s.s1;
+        S.part[k][1][o] = s.s2;
+        S.part[k][2][o] = s.sp;
+        S.part[k][3][o] = s.spp;
+    }
+    group_sync(g);
+    // f. warp 0: children's fitness, best key, next histogram
+    if (k == 0) {
+        const bool active = o < noff;
+        int64_t value = 0;
+        if (active) {
+            Sums s{0, 0, 0, 0};
+#pragma unroll
+            for (int kk = 0; kk < kTeam; ++kk) {
+                s.s1 += S.part[kk][0][o];
+                s.s2 += S.part[kk][1][o];
+                s.sp += S.part[kk][2][o];
+                s.spp += S.part[kk][3][o];
+            }
+            value = variant_value<M, VM>(s, G::NP);
+            const int64_t slot = 2 * N + (int64_t)(o & 1) * N + p0 + (o >> 1);
+            f_new[slot] = value;
+            L.best = min(L.best, ((unsigned long long)value << 32) | (unsigned long long)slot);
+        }
+        local_hist_add(L, ws, gp ^ 1, active, (uint32_t)(value >> gshift));
+    }
+    // g. coalesced store of the children (O1 block, then O2 block)
+    for (int x = t; x < noff * G::U; x += kR2Threads) {
+        const int b = x / (cnt * G::U);
+        const int r = x - b * cnt * G::U;
+        const int q = r / G::U, u = r - q * G::U;
+        reinterpret_cast<uint4*>(pop_new + (2 * N + (int64_t)b * N + p0 + q) * G::MW)[u] = rows[(2 * q + b) * G::STU + u];
+    }
+    group_sync(g);
+}
+
+constexpr int kMaxNb = 512;  // prefix scan: one pass of <= 16 warps
+
+template <int M, int VM, int GROUPS>
+__global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t sscr[32];
+    __shared__ int s_bin;
+    __shared__ uint64_t s_below;
+    __shared__ TileShared S[GROUPS];
+    __shared__ uint32_t s_hist[kWin];
+    __shared__ uint32_t s_kmin, s_kmax;
+    __shared__ unsigned long long s_best, s_pbest;
+    __shared__ uint32_t s_ltpre[kMaxNb + 1], s_eqpre[kMaxNb + 1];
+
+    using G = RunGeom<M>;
+    const hga_run_args& A = P.a;
+    RunWs2* ws = reinterpret_cast<RunWs2*>(A.ws);
+    int32_t* lt_list = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(A.ws) + run_ws2_head());
+    const int64_t N = A.n_pairs, half = 2 * N, total = 4 * N;
+    int32_t* eq_list = lt_list + total;
+    const int nb = gridDim.x, bid = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    const int g = tid / kR2Threads;
+    const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    const int64_t chunk = (((total + nb - 1) / nb) + kSelItems - 1) / kSelItems * kSelItems;
+    const int64_t lo = min(total, (int64_t)bid * chunk), hi = min(total, lo + chunk);
+    const int nc = A.strategy == HGA_MUT_MULTI ? A.nc : 1;
+    const int nr = A.strategy == HGA_MUT_MULTI ? A.nr : 1;
+    const int gshift = P.gshift;
+    const int64_t ntiles = (N + kR2Pairs - 1) / kR2Pairs;
+    // warps taking part in the select scans (the rest only meet the barriers)
+    const int pw_sel = (int)min((int64_t)nw, (chunk / kSelItems + 31) / 32);
+    const int pw_pre = (nb + 31) / 32;  // nb <= kMaxNb = 32 * 32
+    uint4* rows = reinterpret_cast<uint4*>(smem) + (size_t)g * kTileOff * G::STU;
+
+    int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
+    int parity = (int)A.state[3];
+    int64_t run = A.state[6], last_val = A.state[7];
+    const bool force = (A.flags & HGA_RUN_FORCE) != 0;
+    bool stop = !force && A.state[5] != 0;
+    const bool timing = (A.flags & HGA_RUN_TIMING) != 0 && bid == 0 && tid == 0;
+
+    for (int64_t gi = 0; gi < A.gens_this_call && !stop; ++gi) {
+        const int64_t gen = iter + 1;
+        const int gp = (int)(gen & 1);  // histogram / key slot of the population entering `gen`
+        const uint32_t* pop_old = A.pop[parity];
+        uint32_t* pop_new = A.pop[parity ^ 1];
+        const int64_t* f_old = A.fit[parity];
+        int64_t* f_new = A.fit[parity ^ 1];
+        if (timing && gi < 64) {
+            ws->tstamp[gi][0] = gtimer();
+            ws->tstamp[gi][10] = clock64();
+        }
+
+        // ---- B: threshold, tie quota, local survivor lists
+        const uint32_t kmin = __ldcg(&ws->kmin[gp]), kmax = __ldcg(&ws->kmax[gp]);
+        if (wid == 0) kth_bin_warp(&ws->hist[gp][kmin], (int)(kmax - kmin + 1), (uint64_t)half, &s_bin, &s_below);
+        __syncthreads();
+        const int64_t tau = (int64_t)(kmin + (uint32_t)s_bin) << gshift;
+        const uint32_t quota = (uint32_t)((uint64_t)half - s_below);
+        {
+            uint32_t lt_run = 0, eq_run = 0;
+            const int64_t span = (int64_t)pw_sel * 32 * kSelItems;
+            for (int64_t b0 = lo; b0 < hi; b0 += span) {
+                const int64_t i0 = b0 + (int64_t)tid * kSelItems;
+                int64_t f[kSelItems];
+                uint32_t v = 0, x = 0;
+                if (wid < pw_sel) {
+                    load_items(f_old, i0, hi, f);
+#pragma unroll
+                    for (int u = 0; u < kSelItems; ++u) {
+                        const bool in = i0 + u < hi;
+                        v += (in && f[u] < tau) ? 0x10000u : 0u;
+                        v += (in && f[u] == tau) ? 1u : 0u;
+                    }
+                    x = v;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    if (lane == 31) sscr[wid] = x;
+                }
+                __syncthreads();
+                uint32_t wbase = 0, tot = 0;
+                for (int w = 0; w < pw_sel; ++w) {
+                    const uint32_t tw = (uint32_t)sscr[w];
+                    if (w < wid) wbase += tw;
+                    tot += tw;
+                }
+                if (wid < pw_sel) {
+                    uint32_t excl = wbase + x - v;
+#pragma unroll
+                    for (int u = 0; u < kSelItems; ++u) {
+                        const bool in = i0 + u < hi;
+                        if (in && f[u] < tau) lt_list[lo + lt_run + (excl >> 16)] = (int32_t)(i0 + u);
+                        if (in && f[u] == tau) eq_list[lo + eq_run + (excl & 0xffffu)] = (int32_t)(i0 + u);
+                        excl += ((in && f[u] < tau) ? 0x10000u : 0u) + ((in && f[u] == tau) ? 1u : 0u);
+                    }
+                }
+                lt_run += tot >> 16;
+                eq_run += tot & 0xffffu;
+                __syncthreads();
+            }
+            if (tid == 0) {
+                ws->cnt_lt[bid] = lt_run;
+                ws->cnt_eq[bid] = eq_run;
+            }
+        }
+        if (timing && gi < 64) ws->tstamp[gi][1] = gtimer();
+        grid_sync(&ws->bar);
+        if (timing && gi < 64) ws->tstamp[gi][2] = gtimer();
+
+        // ---- E: prefix of the survivor counts, then the offspring tiles
+        if (bid == 0) {
+            for (uint32_t b = kmin + tid; b <= kmax; b += nt) ws->hist[gp][b] = 0;
+        }
+        {
+            // exclusive prefix of cnt_lt / cnt_eq over the nb CTAs (nb <= kMaxNb), pw_pre warps
+            uint64_t x = 0, v = 0;
+            const int b = tid;
+            if (wid < pw_pre) {
+                const uint32_t a = b < nb ? __ldcg(&ws->cnt_lt[b]) : 0u;
+                const uint32_t e = b < nb ? __ldcg(&ws->cnt_eq[b]) : 0u;
+                x = v = ((uint64_t)a << 32) | e;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (lane == 31) sscr[wid] = x;
+            }
+            __syncthreads();
+            if (wid < pw_pre) {
+                uint64_t wbase = 0, tot = 0;
+                for (int w = 0; w < pw_pre; ++w) {
+                    if (w < wid) wbase += sscr[w];
+                    tot += sscr[w];
+                }
+                const uint64_t excl = wbase + x - v;
+                if (b < nb) {
+                    s_ltpre[b] = (uint32_t)(excl >> 32);
+                    s_eqpre[b] = (uint32_t)(excl & 0xffffffffu);
+                }
+                if (tid == 0) {
+                    s_ltpre[nb] = (uint32_t)(tot >> 32);
+                    s_eqpre[nb] = (uint32_t)(tot & 0xffffffffu);
+                }
+            }
+        }
+        LocalAcc L;
+        L.s_hist = s_hist;
+        L.wbase = kmin > 256u ? kmin - 256u : 0u;
+        L.kmin = 0xffffffffu;
+        L.kmax = 0u;
+        L.best = ~0ull;
+        L.pbest = ~0ull;
+        for (int b = tid; b < kWin; b += nt) s_hist[b] = 0;
+        if (tid == 0) {
+            s_kmin = 0xffffffffu;
+            s_kmax = 0u;
+            s_best = ~0ull;
+            s_pbest = ~0ull;
+        }
+        __syncthreads();
+        SelView V{s_ltpre, s_eqpre, nb, chunk, lt_list, eq_list, s_ltpre[nb]};
+        const FeistelKey fkey = make_feistel_key(draw4(A.seed, 0, 0, (uint64_t)gen, (uint32_t)kPSelect), (uint32_t)half);
+        if (timing && gi < 64) ws->tstamp[gi][7] = gtimer();
+        for (int64_t tile = (int64_t)bid * GROUPS + g; tile < ntiles; tile += (int64_t)nb * GROUPS) {
+            const int64_t p0 = tile * kR2Pairs;
+            const int cnt = (int)min((int64_t)kR2Pairs, N - p0);
+            offspring_tile_v4<M, VM>(A, ws, V, fkey, pop_old, pop_new, f_old, f_new, p0, cnt, nc, nr, (uint64_t)gen,
+                                     gp, gshift, rows, S[g], L, g);
+        }
+        if (timing && gi < 64) ws->tstamp[gi][8] = gtimer();
+        // flush the CTA's histogram window, key range and best keys
+        {
+            unsigned long long kb = L.best, pb = L.pbest;
+            for (int o = 16; o; o >>= 1) {
+                kb = min(kb, __shfl_xor_sync(0xffffffffu, kb, o));
+                pb = min(pb, __shfl_xor_sync(0xffffffffu, pb, o));
+            }
+            const uint32_t mn = __reduce_min_sync(0xffffffffu, L.kmin);
+            const uint32_t mx = __reduce_max_sync(0xffffffffu, L.kmax);
+            if (lane == 0) {
+                atomicMin(&s_best, kb);
+                atomicMin(&s_pbest, pb);
+                atomicMin(&s_kmin, mn);
+                atomicMax(&s_kmax, mx);
+            }
+            __syncthreads();
+            for (int b = tid; b < kWin; b += nt)
+                if (s_hist[b]) atomicAdd(&ws->hist[gp ^ 1][L.wbase + b], s_hist[b]);
+            if (tid == 0) {
+                if (s_best != ~0ull) atomicMin(&ws->best_key[gp], s_best);
+                if (s_pbest != ~0ull) atomicMin(&ws->par_key[gp], s_pbest);
+                if (s_kmin != 0xffffffffu) atomicMin(&ws->kmin[gp ^ 1], s_kmin);
+                atomicMax(&ws->kmax[gp ^ 1], s_kmax);
+            }
+        }
+        if (timing && gi < 64) ws->tstamp[gi][9] = gtimer();
+        grid_sync(&ws->bar);
+        if (timing && gi < 64) {
+            ws->tstamp[gi][4] = gtimer();
+            ws->tstamp[gi][11] = clock64();
+        }
+
+        // ---- F: bookkeeping (identical in every CTA)
+        {
+            const unsigned long long key = __ldcg(&ws->best_key[gp]);
+            const int64_t v = (int64_t)(key >> 32);
+            const int64_t idx = (int64_t)(key & 0xffffffffu);
+            iter = gen;
+            parity ^= 1;
+            run = (v == last_val) ? run + 1 : 1;
+            last_val = v;
+            const bool improved = v < best;
+            if (improved) best = v;
+            if (bid == 0) {
+                if (gen < A.trace_capacity) A.trace[gen] = v;
+                if (improved) {
+                    for (int64_t t2 = tid; t2 < G::MW; t2 += nt) A.best_matrix[t2] = __ldcg(pop_new + idx * G::MW + t2);
+                    if (tid == 0) A.state[4] = idx;
+                }
+                if (tid == 0) {
+                    ws->best_key[gp ^ 1] = ~0ull;
+                    ws->par_key[gp ^ 1] = ~0ull;
+                    ws->kmin[gp] = 0xffffffffu;
+                    ws->kmax[gp] = 0u;
+                }
+            }
+            stop = !force && (best == 0 || iter >= A.max_generation);
+            if (!stop && !force && A.stall_window > 0 && iter - last_restart >= A.stall_window &&
+                run >= A.stall_window && last_val > 0) {
+                // stall restart (engine.py:482-494): fresh offspring, parents kept,
+                // next-generation histogram rebuilt from scratch
+                const int ngp = gp ^ 1;
+                const uint32_t omin = __ldcg(&ws->kmin[ngp]), omax = __ldcg(&ws->kmax[ngp]);
+                grid_sync(&ws->bar);
+                if (bid == 0) {
+                    for (uint32_t b = omin + tid; b <= omax; b += nt) ws->hist[ngp][b] = 0;
+                    if (tid == 0) {
+                        ws->kmin[ngp] = 0xffffffffu;
+                        ws->kmax[ngp] = 0u;
+                    }
+                }
+                const int64_t work = half * M;
+                for (int64_t t0 = (int64_t)bid * nt; t0 < work; t0 += (int64_t)nb * nt) {
+                    const int64_t tt = t0 + tid;
+                    if (tt < work) {
+                        const int64_t s = half + tt / M;
+                        const int c = (int)(tt % M);
+                        Col<G::W> col;
+                        philox_column<G::W>(A.seed, (uint32_t)kPRestart, (uint64_t)iter, s, M, c, col);
+#pragma unroll
+                        for (int w = 0; w < G::W; ++w) pop_new[s * G::MW + (int64_t)c * G::W + w] = col.w[w];
+                    }
+                }
+                grid_sync(&ws->bar);
+                // evaluate all 4N (fresh offspring; parents unchanged) and rebuild the histogram
+                for (int64_t k0 = (int64_t)bid * nt; k0 < total; k0 += (int64_t)nb * nt) {
+                    const int64_t k = k0 + tid;
+                    const bool ok = k < total;
+                    int64_t fv = 0;
+                    if (ok) {
+                        if (k >= half) {
+                            uint32_t c[G::MW];
+#pragma unroll
+                            for (int u = 0; u < G::U; ++u) {
+                                const uint4 v4 = __ldcg(reinterpret_cast<const uint4*>(pop_new + k * G::MW) + u);
+                                c[4 * u] = v4.x;
+                                c[4 * u + 1] = v4.y;
+                                c[4 * u + 2] = v4.z;
+                                c[4 * u + 3] = v4.w;
+                            }
+                            Sums s{0, 0, 0, 0};
+                            pair_sums<M, VM, 1>(c, s);
+                            fv = variant_value<M, VM>(s, G::NP);
+                            f_new[k] = fv;
+                        } else {
+                            fv = __ldcg(f_new + k);
+                        }
+                    }
+                    hist_add(ws, ngp, ok, (uint32_t)(fv >> gshift));
+                    key_min_warp(&ws->restart_key,
+                                 ok && k >= half ? (((unsigned long long)fv << 32) | (unsigned long long)k) : ~0ull);
+                }
+                grid_sync(&ws->bar);
+                const unsigned long long rk = __ldcg(&ws->restart_key);
+                const unsigned long long pk = __ldcg(&ws->par_key[gp]);
+                const unsigned long long k2 = min(rk, pk);
+                const int64_t v2 = (int64_t)(k2 >> 32);
+                if (v2 < best) {
+                    best = v2;
+                    if (bid == 0) {
+                        const int64_t id2 = (int64_t)(k2 & 0xffffffffu);
+                        for (int64_t t2 = tid; t2 < G::MW; t2 += nt) A.best_matrix[t2] = __ldcg(pop_new + id2 * G::MW + t2);
+                        if (tid == 0) A.state[4] = id2;
+                    }
+                }
+                last_restart = iter;
+                grid_sync(&ws->bar);
+                if (bid == 0 && tid == 0) ws->restart_key = ~0ull;
+                stop = best == 0;
+            }
+        }
+    }
+    if (bid == 0 && tid == 0) {
+        A.state[0] = iter;
+        A.state[1] = best;
+        A.state[2] = last_restart;
+        A.state[3] = parity;
+        A.state[5] = (best == 0 || iter >= A.max_generation) ? 1 : 0;
+        A.state[6] = run;
+        A.state[7] = last_val;
+    }
+}
+
+int run2_granule_shift(uint32_t fit_var);
+bool run2_supported(const hga_run_args* a);
+
+template <int M>
+int launch_run_v2_m(const hga_run_args* a, cudaStream_t st);
+
+#define HGA_R2_ORDERS(X) X(4) X(8) X(12) X(16) X(20) X(24) X(28) X(32) X(36) X(40) X(44) X(48) X(52) X(56) X(60) X(64)
+#define HGA_R2_EXTERN(M) extern template int launch_run_v2_m<M>(const hga_run_args*, cudaStream_t);
+
+template <int M>
+constexpr int run_groups() {
+    return M <= 36 ? 4 : 2;  // 512 threads need <= 128 registers per thread
+}
+
+// Definition used by the per-order instantiation files run_m<M>.cu.
+template <int M, int VM>
+int launch_run_v2_mv(const hga_run_args* a, cudaStream_t st) {
+    constexpr int GROUPS = run_groups<M>();
+    Run2Params P;
+    P.a = *a;
+    P.gshift = run2_granule_shift(a->fit_var);
+    const int smem = GROUPS * kTileOff * RunGeom<M>::STU * 16;
+    auto kern = k_run_v3<M, VM, GROUPS>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return to_rc(e);
+        attr = true;
+    }
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kR2Threads * GROUPS, smem);
+        if (e != cudaSuccess) return to_rc(e);
+    }
+    if (per_sm < 1) return HGA_E_UNSUPPORTED;
+    const int grid = std::min(std::min(sm_count_cached() * std::min(per_sm, 2), kMaxNb), GROUPS * kR2Threads);
+    void* params[] = {&P};
+    return to_rc(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kR2Threads * GROUPS), params, smem, st));
+}
+
+template <int M>
+int launch_run_v2_m(const hga_run_args* a, cudaStream_t st) {
+    switch (a->fit_var) {
+        case HGA_VAR_F1: return launch_run_v2_mv<M, HGA_VAR_F1>(a, st);
+        case HGA_VAR_SQ:
+            if constexpr (M <= 32) return launch_run_v2_mv<M, HGA_VAR_SQ>(a, st);
+            return HGA_E_UNSUPPORTED;
+        default: return launch_run_v2_mv<M, HGA_VAR_F2>(a, st);
+    }
+}
+
+}  // namespace hga

@@ -726,6 +726,7 @@ def _step_host(state):
     res.dstate.copy_(torch.tensor([inner.iteration, inner.best_fitness, 0, cur, 0, 0, 1, inner.trace[-1]],
                                   dtype=torch.int64), non_blocking=True)
     inner.best_matrix = None
+    check(lib.hga_run_prepare(res.run_args(), stream_ptr()), "hga_run_prepare") if bridge.cfg.rng == "philox" else None
     step(inner)
     check(lib.hga_unpack_i8(res.pop[res.cur].data_ptr(), total, m, bridge.pop_i8.data_ptr(), stream_ptr()),
           "hga_unpack_i8")

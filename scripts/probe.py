@@ -117,8 +117,12 @@ def probe_ga():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", choices=("pipes", "fitness", "ga"), default=None)
     args = ap.parse_args()
     print(json.dumps({"device": torch.cuda.get_device_name(0)}), flush=True)
-    probe_pipes()
-    probe_fitness(args.quick)
-    probe_ga()
+    if args.only in (None, "pipes"):
+        probe_pipes()
+    if args.only in (None, "fitness"):
+        probe_fitness(args.quick)
+    if args.only in (None, "ga"):
+        probe_ga()

@@ -25,9 +25,11 @@ def main():
     ap.add_argument("--gens", type=int, default=6)
     ap.add_argument("--fitness-m", type=int, default=20)
     ap.add_argument("--fitness-n", type=int, default=4_000_000)
+    ap.add_argument("--ga-m", type=int, default=20)
+    ap.add_argument("--ga-n", type=int, default=10_000)
     args = ap.parse_args()
     sp = torch.cuda.current_stream().cuda_stream
-    cfg = engine.GAConfig(order=20, population=10_000, seed=2024, fitness="f2", mutation_cols=4, mutation_row_pairs=2,
+    cfg = engine.GAConfig(order=args.ga_m, population=args.ga_n, seed=2024, fitness="f2", mutation_cols=4, mutation_row_pairs=2,
                           max_iterations=engine.MAX_ITERATIONS)
     st = hga.initial_state(cfg)
     res = st._res
