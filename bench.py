@@ -42,6 +42,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 ORDER, N_PAIRS, FITNESS, NC, NR = 20, 10_000, "f2", 4, 2
+MIGRATE_EVERY, MIGRATION_SIZE = 50, 16  # islands (n_gpus > 1): ring migration of 16 elites every 50 generations
 METRIC = "matrix fitness evals/sec (order-20 GA generation, 40,000 matrices, 2N offspring evaluated per generation)"
 UNIT = "evals/s"
 
@@ -142,10 +143,20 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
 
-    cfg = engine.GAConfig(order=ORDER, population=N_PAIRS, seed=2024 + rank, fitness=FITNESS, mutation_cols=NC,
+    from paper_2208_14961_b200.islands import Exchange, GpuIsland, island_seed, pack_payload, unpack_payload
+
+    cfg = engine.GAConfig(order=ORDER, population=N_PAIRS, seed=2024, fitness=FITNESS, mutation_cols=NC,
                           mutation_row_pairs=NR, max_iterations=engine.MAX_ITERATIONS)
-    st = hga.initial_state(cfg)
+    island = GpuIsland(cfg, island_seed(2024, rank))
+    st = island.state
     res = st._res
+    ex = Exchange() if world > 1 else None
+
+    def migrate():
+        # ring elite migration (islands.py): E best -> next island's offspring slots
+        rec, fit = island.elites(MIGRATION_SIZE)
+        r2, f2 = unpack_payload(ex.ring_shift(pack_payload(rec, fit)), MIGRATION_SIZE, rec.shape[1])
+        island.receive(r2, f2)
     res.ensure_trace(args.warmup + args.steps + 8)
     a = res.run_args()
     a.gens_this_call = 1
@@ -174,10 +185,12 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     wall0 = time.perf_counter()
-    for s, e in evs:
+    for i, (s, e) in enumerate(evs):
         flush.fill_(1)  # write 256 MiB > 126 MB L2 between timed steps
         s.record(stream)
         one_generation()
+        if ex is not None and (i + 1) % MIGRATE_EVERY == 0:
+            migrate()  # the exchange step of the island model, inside the timed step
         e.record(stream)
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
@@ -246,9 +259,11 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": "BASELINE configs[1]: order-20 GA, population 40,000 matrices (N=10,000 pairs), "
                                "fitness f2, mutation multi NC=4 NR=2, rng philox",
                    "order": ORDER, "matrices": 4 * N_PAIRS, "offspring_evals_per_step": evals_per_step,
-                   "parallelism": f"islands x{world} (one independent population per GPU)",
+                   "parallelism": f"islands x{world} (one 40,000-matrix population per GPU"
+                                  + (f"; NCCL ring migration of {MIGRATION_SIZE} elites every {MIGRATE_EVERY} steps)"
+                                     if world > 1 else ")"),
                    "l2": "flushed between timed steps (256 MiB write, outside the CUDA events)"},
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps + (5 * (args.steps // MIGRATE_EVERY) if world > 1 else 0),
         "roofline": roofline,
         "e2e": e2e,
         "persistent_run": {"value": persistent * world, "unit": UNIT, "generations_per_launch": args.steps,

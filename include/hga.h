@@ -131,6 +131,10 @@ int64_t hga_select_max_range(void);
 size_t hga_select_ws_bytes(int64_t total);
 int hga_select_order(const int64_t *fitness, int64_t total, int64_t *order, int32_t *bad_flag,
                      void *ws, size_t ws_bytes, void *stream);
+/* order[0:k] = argsort(fitness, stable)[:k] (k <= total): the k best,
+ * lowest index first on ties; used for island elites. */
+int hga_select_smallest(const int64_t *fitness, int64_t total, int64_t k, int64_t *order,
+                        int32_t *bad_flag, void *ws, size_t ws_bytes, void *stream);
 /* chosen[s] = order[perm[s]] (s < count); then gathers rows
  * dst[s] = src[chosen[s]] (layout bytes per matrix given) and
  * fit_dst[s] = fit_src[chosen[s]] (either may be NULL). */

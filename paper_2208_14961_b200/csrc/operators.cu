@@ -264,7 +264,13 @@ size_t hga_select_ws_bytes(int64_t total) {
 int hga_select_order(const int64_t* fitness, int64_t total, int64_t* order, int32_t* bad_flag, void* ws,
                      size_t ws_bytes, void* stream) {
     if (total < 0) return HGA_E_INVALID;
-    const int64_t half = total / 2;
+    return hga_select_smallest(fitness, total, total / 2, order, bad_flag, ws, ws_bytes, stream);
+}
+
+int hga_select_smallest(const int64_t* fitness, int64_t total, int64_t k, int64_t* order, int32_t* bad_flag,
+                        void* ws, size_t ws_bytes, void* stream) {
+    if (total < 0 || k < 0 || k > total) return HGA_E_INVALID;
+    const int64_t half = k;
     if (half == 0) return HGA_OK;
     if (!ws || ws_bytes < hga_select_ws_bytes(total)) return HGA_E_WORKSPACE;
     cudaStream_t st = (cudaStream_t)stream;

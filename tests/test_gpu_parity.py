@@ -311,3 +311,28 @@ def test_philox_stall_restart_runs(cuda_device):
     rec = hga.run_search(cfg)
     assert all(a >= b for a, b in zip(rec.trace, rec.trace[1:]))
     assert rec.best_fitness == rec.trace[-1] or rec.best_fitness <= rec.trace[-1]
+
+
+def test_single_gpu_island_and_elites(cuda_device):
+    from paper_2208_14961_b200.islands import GpuIsland, IslandConfig, run_islands
+
+    rec = run_islands(engine.GAConfig(order=12, population=1000, seed=3, fitness="f1", max_iterations=3000),
+                      IslandConfig(migration_interval=50, migration_size=8, poll_interval=25))
+    assert rec.success and rec.world == 1
+    q = rec.best_matrix.astype(np.int64)
+    assert (q.T @ q == 12 * np.eye(12, dtype=np.int64)).all()
+    isl = GpuIsland(engine.GAConfig(order=20, population=500, seed=9), seed=9)
+    isl.advance(3)
+    fit = isl.state.fitness
+    rec_e, fit_e = isl.elites(16)
+    order = np.argsort(fit, kind="stable")[:16]
+    assert np.array_equal(fit_e.cpu().numpy(), fit[order])
+    pop = isl.state.population
+    assert np.array_equal(engine._unpack(rec_e.reshape(-1), 16, 20).cpu().numpy(), pop[order])
+    # migrants land in the first offspring slots and the loop keeps running
+    isl.receive(rec_e, fit_e)
+    after = isl.state.population
+    assert np.array_equal(after[1000:1016], pop[order])
+    isl.advance(2)
+    p2 = isl.state.population
+    assert np.array_equal(isl.state.fitness, oracle.evaluate(p2, "f2"))
