@@ -202,7 +202,7 @@ int hga_philox_init_packed(uint64_t seed, uint64_t purpose, uint64_t generation,
                            void *stream);
 
 size_t hga_run_ws_bytes(int64_t n_pairs, int32_t m);
-/* byte offset inside ws of the uint64 [64][12] phase timestamps (HGA_RUN_TIMING),
+/* byte offset inside ws of the uint64 [64][20] phase timestamps (HGA_RUN_TIMING),
  * or -1 when the order runs on the fallback loop */
 int64_t hga_run_timing_offset(int32_t m);
 /* Philox-stream init of all 4N slots of pop[0] + evaluation + state init. */

@@ -677,7 +677,7 @@ int hga_generation_explicit(uint32_t* pop, int64_t* fit, int64_t n_pairs, int32_
 
 size_t hga_run_ws_bytes(int64_t n_pairs, int32_t m) {
     (void)m;
-    return std::max(run_ws_head() + (size_t)(2 * n_pairs) * 8, run_ws2_head() + (size_t)(8 * n_pairs) * 4);
+    return std::max(run_ws_head() + (size_t)(2 * n_pairs) * 8, run_ws2_head() + (size_t)(8 * n_pairs) * 8);
 }
 
 

@@ -47,8 +47,8 @@ struct RunWs2 {
     uint32_t cnt_lt[kR2MaxGrid];
     uint32_t cnt_eq[kR2MaxGrid];
     uint32_t hist[2][kR2Bins];
-    unsigned long long tstamp[64][12];  // HGA_RUN_TIMING: %globaltimer at phase boundaries (CTA 0)
-    // followed by lt_list[4N], eq_list[4N] (int32): each CTA's survivors, compacted in index order
+    unsigned long long tstamp[64][20];  // HGA_RUN_TIMING: %globaltimer at phase boundaries (CTA 0)
+    // followed by lt_list[4N], eq_list[4N] (uint64 (F << 32) | index): each CTA's survivors, compacted in index order
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -211,13 +211,13 @@ __device__ __forceinline__ void load_items(const int64_t* f, int64_t i0, int64_t
     }
 }
 
-// Keyed bijection on [0, n): six alternating xor-rounds on a (bl | br)-bit
-// split of the smallest power-of-two domain >= n, plus cycle walking
-// (domain < 2n, so fewer than two walks on average).
+// Keyed bijection on [0, n): a six-round alternating Feistel network on
+// Z_a x Z_b with a = ceil(sqrt n), b = ceil(n / a) (each round adds a
+// Lemire-bounded hash of the other half modulo its own radix), plus cycle
+// walking -- the domain a*b < n + b, so almost every point maps in one walk.
 struct FeistelKey {
     uint32_t k[6];
-    uint32_t n;
-    int bl, br;
+    uint32_t n, a, b;
 };
 
 __device__ __forceinline__ FeistelKey make_feistel_key(const U4& r, uint32_t n) {
@@ -228,41 +228,40 @@ __device__ __forceinline__ FeistelKey make_feistel_key(const U4& r, uint32_t n) 
     f.k[3] = r.w;
     f.k[4] = hash32(r.x ^ 0x68E31DA4u);
     f.k[5] = hash32(r.y ^ 0xB5297A4Du);
-    f.n = n;
-    int b = 0;
-    for (uint32_t x = n > 1 ? n - 1 : 1; x; x >>= 1) ++b;
-    b = b < 2 ? 2 : b;
-    f.bl = b / 2;
-    f.br = b - b / 2;
+    f.n = n < 1 ? 1 : n;
+    uint32_t a = (uint32_t)ceilf(sqrtf((float)f.n));
+    while ((uint64_t)a * a < f.n) ++a;
+    f.a = a;
+    f.b = (f.n + a - 1) / a;
     return f;
 }
 
-__device__ __forceinline__ uint32_t feistel2_inv(uint32_t y, const FeistelKey& f) {
-    const uint32_t ml = (1u << f.bl) - 1u, mr = (1u << f.br) - 1u;
-    do {
-        uint32_t L = y >> f.br, R = y & mr;
-#pragma unroll
-        for (int r = 4; r >= 0; r -= 2) {
-            R ^= hash32(L ^ f.k[r + 1]) & mr;
-            L ^= hash32(R ^ f.k[r]) & ml;
-        }
-        y = (L << f.br) | R;
-    } while (y >= f.n);
-    return y;
-}
-
 __device__ __forceinline__ uint32_t feistel2(uint32_t x, const FeistelKey& f) {
-    const uint32_t ml = (1u << f.bl) - 1u, mr = (1u << f.br) - 1u;
+    uint32_t L = x / f.b, R = x - (x / f.b) * f.b;
     do {
-        uint32_t L = x >> f.br, R = x & mr;
 #pragma unroll
         for (int r = 0; r < 6; r += 2) {
-            L ^= hash32(R ^ f.k[r]) & ml;
-            R ^= hash32(L ^ f.k[r + 1]) & mr;
+            L += bounded(hash32(R ^ f.k[r]), f.a);
+            L -= L >= f.a ? f.a : 0u;
+            R += bounded(hash32(L ^ f.k[r + 1]), f.b);
+            R -= R >= f.b ? f.b : 0u;
         }
-        x = (L << f.br) | R;
-    } while (x >= f.n);
-    return x;
+    } while (L * f.b + R >= f.n);
+    return L * f.b + R;
+}
+
+__device__ __forceinline__ uint32_t feistel2_inv(uint32_t y, const FeistelKey& f) {
+    uint32_t L = y / f.b, R = y - (y / f.b) * f.b;
+    do {
+#pragma unroll
+        for (int r = 4; r >= 0; r -= 2) {
+            const uint32_t tr = bounded(hash32(L ^ f.k[r + 1]), f.b);
+            R = R >= tr ? R - tr : R + f.b - tr;
+            const uint32_t tl = bounded(hash32(R ^ f.k[r]), f.a);
+            L = L >= tl ? L - tl : L + f.a - tl;
+        }
+    } while (L * f.b + R >= f.n);
+    return L * f.b + R;
 }
 
 struct Run2Params {
@@ -302,8 +301,8 @@ struct SelView {
     const uint32_t* eq_pre;
     int nb;
     int64_t chunk;
-    const int32_t* lt_list;
-    const int32_t* eq_list;
+    const unsigned long long* lt_list;
+    const unsigned long long* eq_list;
     uint32_t total_lt;
 };
 
@@ -317,7 +316,7 @@ __device__ __forceinline__ int upper_bound_u32(const uint32_t* a, int n, uint32_
     return lo;
 }
 
-__device__ __forceinline__ int32_t survivor_by_rank(const SelView& V, uint32_t r) {
+__device__ __forceinline__ unsigned long long survivor_by_rank(const SelView& V, uint32_t r) {
     if (r < V.total_lt) {
         const int b = upper_bound_u32(V.lt_pre, V.nb + 1, r) - 1;
         return __ldcg(V.lt_list + (int64_t)b * V.chunk + (r - V.lt_pre[b]));
@@ -340,7 +339,8 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
                                                   uint32_t* __restrict__ pop_new, const int64_t* __restrict__ f_old,
                                                   int64_t* __restrict__ f_new, int64_t p0, int cnt, int nc, int nr,
                                                   uint64_t gen, int gp, int gshift, uint4* rows, TileShared& S,
-                                                  LocalAcc& L, int g) {
+                                                  LocalAcc& L, int g, unsigned long long* ts) {
+    const bool tm = ts != nullptr && (threadIdx.x & (kR2Threads - 1)) == 0;
     using G = RunGeom<M>;
     constexpr int W = G::W;
     const int64_t N = A.n_pairs;
@@ -349,43 +349,46 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
     const int per_off = nc + 2 * nr;
     const int nblk = (per_off + 3) >> 2;
 
-    // a. crossover points, parents (select: slot -> rank -> survivor), Philox plans
-    if (t < cnt) {
-        const int64_t p = p0 + t;
-        const U4 r = draw4(A.seed, (uint32_t)p, (uint32_t)(p >> 32), gen, (uint32_t)kPCrossover);
-        S.point[t] = (int16_t)(1 + bounded(r.x, (uint32_t)(M - 1)));
-    }
+    // a. warp 0: parents (select: slot -> rank -> survivor); warp 3: crossover
+    //    points; warps 1-3: Philox mutation plans
     if (k == 0) {
         const bool act = o < noff;
         int64_t f = 0;
         if (act) {
             const int q = o >> 1, b = o & 1;
             const int64_t slot = (int64_t)b * N + p0 + q;
-            const int32_t idx = survivor_by_rank(V, feistel2_inv((uint32_t)slot, fkey));
-            S.pidx[o] = idx;
-            f = __ldcg(f_old + idx);
+            const unsigned long long kv = survivor_by_rank(V, feistel2_inv((uint32_t)slot, fkey));
+            S.pidx[o] = (int32_t)(kv & 0xffffffffu);
+            f = (int64_t)(kv >> 32);
             f_new[slot] = f;
             const unsigned long long key = ((unsigned long long)f << 32) | (unsigned long long)slot;
             L.best = min(L.best, key);
             L.pbest = min(L.pbest, key);
         }
         local_hist_add(L, ws, gp ^ 1, act, (uint32_t)(f >> gshift));
-    }
-    for (int x = t; x < noff * nblk; x += kR2Threads) {
-        const int ol = x / nblk, blk = x - (x / nblk) * nblk;
-        const int q = ol >> 1;
-        int64_t prow = (ol & 1) ? N + p0 + q : p0 + q;  // plan row as engine.py: O1 -> p, O2 -> N + p
-        if (A.strategy == HGA_MUT_SHARED) prow = 0;
-        const U4 r = draw4(A.seed, (uint32_t)prow, (uint32_t)blk | ((uint32_t)(prow >> 32) << 16), gen,
-                           (uint32_t)kPMutCol);
+    } else {
+        if (k == kTeam - 1 && o < cnt) {
+            const int64_t p = p0 + o;
+            const U4 r = draw4(A.seed, (uint32_t)p, (uint32_t)(p >> 32), gen, (uint32_t)kPCrossover);
+            S.point[o] = (int16_t)(1 + bounded(r.x, (uint32_t)(M - 1)));
+        }
+        for (int x = t - 32; x < noff * nblk; x += kR2Threads - 32) {
+            const int ol = x / nblk, blk = x - (x / nblk) * nblk;
+            const int q = ol >> 1;
+            int64_t prow = (ol & 1) ? N + p0 + q : p0 + q;  // plan row as engine.py: O1 -> p, O2 -> N + p
+            if (A.strategy == HGA_MUT_SHARED) prow = 0;
+            const U4 r = draw4(A.seed, (uint32_t)prow, (uint32_t)blk | ((uint32_t)(prow >> 32) << 16), gen,
+                               (uint32_t)kPMutCol);
 #pragma unroll
-        for (int e4 = 0; e4 < 4; ++e4) {
-            const int e = blk * 4 + e4;
-            if (e < per_off)
-                S.plan[ol][e] = (int8_t)(e < nc ? 1 + bounded(pick(r, e4), (uint32_t)(M - 1))
-                                                : bounded(pick(r, e4), (uint32_t)M));
+            for (int e4 = 0; e4 < 4; ++e4) {
+                const int e = blk * 4 + e4;
+                if (e < per_off)
+                    S.plan[ol][e] = (int8_t)(e < nc ? 1 + bounded(pick(r, e4), (uint32_t)(M - 1))
+                                                    : bounded(pick(r, e4), (uint32_t)M));
+            }
         }
     }
+    if (tm) ts[12] = gtimer();
     group_sync(g);
     // b. gather the parents; write them to the new population's parent slots
     for (int x = t; x < noff * G::U; x += kR2Threads) {
@@ -397,6 +400,7 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
         rows[pi * G::STU + u] = v;
         reinterpret_cast<uint4*>(pop_new + ((int64_t)b * N + p0 + q) * G::MW)[u] = v;
     }
+    if (tm) ts[13] = gtimer();
     group_sync(g);
     // c. column-block crossover in place
     for (int x = t; x < cnt * M; x += kR2Threads) {
@@ -412,27 +416,38 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
             }
         }
     }
+    if (tm) ts[14] = gtimer();
     group_sync(g);
-    // d. mutation: warp k applies, in plan order, the entries whose column is k mod 4
+    // d. mutation: thread (k, o) handles plan entries jc = k, k + 4, ...; an
+    //    entry whose column already appeared earlier is skipped, and the first
+    //    occurrence applies the column's row-pair sequence once per occurrence
+    //    (plan order per column == the reference's sequential order)
     if (o < noff) {
         uint32_t* row = reinterpret_cast<uint32_t*>(rows + o * G::STU);
         const int8_t* pl = S.plan[o];
-        for (int jc = 0; jc < nc; ++jc) {
+        for (int jc = k; jc < nc; jc += kTeam) {
             const int col = pl[jc];
-            if ((col & (kTeam - 1)) != k) continue;
+            bool first = true;
+            for (int j2 = 0; j2 < jc; ++j2) first &= pl[j2] != col;
+            if (!first) continue;
+            int reps = 1;
+            for (int j2 = jc + 1; j2 < nc; ++j2) reps += pl[j2] == col;
             uint32_t* cw = row + col * W;
-            for (int ir = 0; ir < nr; ++ir) {
-                const int ra = pl[nc + ir], rb = pl[nc + nr + ir];
-                uint32_t* wa = cw + (ra >> 5);
-                uint32_t* wb = cw + (rb >> 5);
-                const uint32_t xa = (*wa >> (ra & 31)) & 1u, xb = (*wb >> (rb & 31)) & 1u;
-                if (xa != xb) {
-                    *wa ^= 1u << (ra & 31);
-                    *wb ^= 1u << (rb & 31);
+            for (int rep = 0; rep < reps; ++rep) {
+                for (int ir = 0; ir < nr; ++ir) {
+                    const int ra = pl[nc + ir], rb = pl[nc + nr + ir];
+                    uint32_t* wa = cw + (ra >> 5);
+                    uint32_t* wb = cw + (rb >> 5);
+                    const uint32_t xa = (*wa >> (ra & 31)) & 1u, xb = (*wb >> (rb & 31)) & 1u;
+                    if (xa != xb) {
+                        *wa ^= 1u << (ra & 31);
+                        *wb ^= 1u << (rb & 31);
+                    }
                 }
             }
         }
     }
+    if (tm) ts[15] = gtimer();
     group_sync(g);
     // e. pair chain, a quarter per warp
     if (o < noff) {
@@ -457,6 +472,7 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
         S.part[k][2][o] = s.sp;
         S.part[k][3][o] = s.spp;
     }
+    if (tm) ts[16] = gtimer();
     group_sync(g);
     // f. warp 0: children's fitness, best key, next histogram
     if (k == 0) {
@@ -478,6 +494,7 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
         }
         local_hist_add(L, ws, gp ^ 1, active, (uint32_t)(value >> gshift));
     }
+    if (tm) ts[17] = gtimer();
     // g. coalesced store of the children (O1 block, then O2 block)
     for (int x = t; x < noff * G::U; x += kR2Threads) {
         const int b = x / (cnt * G::U);
@@ -486,6 +503,7 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
         reinterpret_cast<uint4*>(pop_new + (2 * N + (int64_t)b * N + p0 + q) * G::MW)[u] = rows[(2 * q + b) * G::STU + u];
     }
     group_sync(g);
+    if (tm) ts[18] = gtimer();
 }
 
 constexpr int kMaxNb = 512;  // prefix scan: one pass of <= 16 warps
@@ -505,9 +523,9 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     using G = RunGeom<M>;
     const hga_run_args& A = P.a;
     RunWs2* ws = reinterpret_cast<RunWs2*>(A.ws);
-    int32_t* lt_list = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(A.ws) + run_ws2_head());
+    unsigned long long* lt_list = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(A.ws) + run_ws2_head());
     const int64_t N = A.n_pairs, half = 2 * N, total = 4 * N;
-    int32_t* eq_list = lt_list + total;
+    unsigned long long* eq_list = lt_list + total;
     const int nb = gridDim.x, bid = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
     const int g = tid / kR2Threads;
     const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
@@ -542,6 +560,9 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
         }
 
         // ---- B: threshold, tie quota, local survivor lists
+        // first batch of fitness values: independent of tau, so load it under the histogram scan
+        int64_t fpre[kSelItems];
+        if (wid < pw_sel) load_items(f_old, lo + (int64_t)tid * kSelItems, hi, fpre);
         const uint32_t kmin = __ldcg(&ws->kmin[gp]), kmax = __ldcg(&ws->kmax[gp]);
         if (wid == 0) kth_bin_warp(&ws->hist[gp][kmin], (int)(kmax - kmin + 1), (uint64_t)half, &s_bin, &s_below);
         __syncthreads();
@@ -555,7 +576,12 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
                 int64_t f[kSelItems];
                 uint32_t v = 0, x = 0;
                 if (wid < pw_sel) {
-                    load_items(f_old, i0, hi, f);
+                    if (b0 == lo) {
+#pragma unroll
+                        for (int u = 0; u < kSelItems; ++u) f[u] = fpre[u];
+                    } else {
+                        load_items(f_old, i0, hi, f);
+                    }
 #pragma unroll
                     for (int u = 0; u < kSelItems; ++u) {
                         const bool in = i0 + u < hi;
@@ -581,8 +607,9 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
 #pragma unroll
                     for (int u = 0; u < kSelItems; ++u) {
                         const bool in = i0 + u < hi;
-                        if (in && f[u] < tau) lt_list[lo + lt_run + (excl >> 16)] = (int32_t)(i0 + u);
-                        if (in && f[u] == tau) eq_list[lo + eq_run + (excl & 0xffffu)] = (int32_t)(i0 + u);
+                        const unsigned long long kv = ((unsigned long long)f[u] << 32) | (unsigned long long)(i0 + u);
+                        if (in && f[u] < tau) lt_list[lo + lt_run + (excl >> 16)] = kv;
+                        if (in && f[u] == tau) eq_list[lo + eq_run + (excl & 0xffffu)] = kv;
                         excl += ((in && f[u] < tau) ? 0x10000u : 0u) + ((in && f[u] == tau) ? 1u : 0u);
                     }
                 }
@@ -656,8 +683,10 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
         for (int64_t tile = (int64_t)bid * GROUPS + g; tile < ntiles; tile += (int64_t)nb * GROUPS) {
             const int64_t p0 = tile * kR2Pairs;
             const int cnt = (int)min((int64_t)kR2Pairs, N - p0);
+            unsigned long long* ts = (A.flags & HGA_RUN_TIMING) != 0 && bid == 0 && g == 0 && gi < 64 &&
+                                             tile == (int64_t)bid * GROUPS + g ? ws->tstamp[gi] : nullptr;
             offspring_tile_v4<M, VM>(A, ws, V, fkey, pop_old, pop_new, f_old, f_new, p0, cnt, nc, nr, (uint64_t)gen,
-                                     gp, gshift, rows, S[g], L, g);
+                                     gp, gshift, rows, S[g], L, g, ts);
         }
         if (timing && gi < 64) ws->tstamp[gi][8] = gtimer();
         // flush the CTA's histogram window, key range and best keys
@@ -814,7 +843,9 @@ int launch_run_v2_m(const hga_run_args* a, cudaStream_t st);
 
 template <int M>
 constexpr int run_groups() {
-    return M <= 36 ? 4 : 2;  // 512 threads need <= 128 registers per thread
+    // tile groups per CTA (one CTA per SM): 640 threads leave <= 102 registers,
+    // 512 threads <= 128; more groups = fewer tiles per group at small N
+    return M <= 24 ? 5 : (M <= 36 ? 4 : 2);
 }
 
 // Definition used by the per-order instantiation files run_m<M>.cu.
