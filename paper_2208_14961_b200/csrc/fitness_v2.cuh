@@ -38,8 +38,13 @@ __device__ __forceinline__ void issue_chunk(int8_t* buf, const int8_t* __restric
     }
 }
 
+template <int M>
+constexpr int i8_min_blocks() {
+    return M > 32 ? 3 : 1;  // cap registers (<= 168) so three CTAs fit per SM at m >= 36
+}
+
 template <int M, int VM>
-__global__ void __launch_bounds__(kV2Threads) k_fit_i8_v2(const int8_t* __restrict__ pop, int64_t n, uint32_t vm_out,
+__global__ void __launch_bounds__(kV2Threads, i8_min_blocks<M>()) k_fit_i8_v2(const int8_t* __restrict__ pop, int64_t n, uint32_t vm_out,
                                                         int64_t* __restrict__ f1, int64_t* __restrict__ f2,
                                                         int64_t* __restrict__ orth, int64_t* __restrict__ sq,
                                                         int32_t* bad_flag) {

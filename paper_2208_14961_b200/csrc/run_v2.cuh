@@ -326,81 +326,104 @@ __device__ __forceinline__ unsigned long long survivor_by_rank(const SelView& V,
     return __ldcg(V.eq_list + (int64_t)b * V.chunk + (e - V.eq_pre[b]));
 }
 
-// Offspring tile of one 128-thread group: pairs [p0, p0 + cnt), cnt <= 16.
-// Parent slot s (p for A, N + p for B) holds the survivor of rank
-// Feistel^-1(s); its row is gathered, copied to slot s of the new population,
-// and -- rows 2q / 2q+1 -- turned into O1 / O2 in place by swapping the
-// columns j >= point (engine.py:257-277).  Children are mutated by column
-// (warp k owns the columns = k mod 4, engine.py:339-373), then each warp runs
-// a quarter of the pair chain of all children.
-template <int M, int VM>
-__device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2* ws, const SelView& V,
-                                                  const FeistelKey& fkey, const uint32_t* __restrict__ pop_old,
-                                                  uint32_t* __restrict__ pop_new, const int64_t* __restrict__ f_old,
-                                                  int64_t* __restrict__ f_new, int64_t p0, int cnt, int nc, int nr,
-                                                  uint64_t gen, int gp, int gshift, uint4* rows, TileShared& S,
-                                                  LocalAcc& L, int g, unsigned long long* ts) {
-    const bool tm = ts != nullptr && (threadIdx.x & (kR2Threads - 1)) == 0;
-    using G = RunGeom<M>;
-    constexpr int W = G::W;
-    const int64_t N = A.n_pairs;
+// One 128-thread tile group runs its tiles (16 pairs -> 32 children each)
+// as a two-stage pipeline: while tile i is crossed, mutated and evaluated,
+// tile i+1's parents are already being gathered with cp.async into the other
+// row buffer.  Parent slot s (p for A, N + p for B) holds the survivor of rank
+// Feistel^-1(s); rows 2q / 2q+1 receive parents A / B of pair q, are copied to
+// the new population's parent slots, and swapping the columns j >= point turns
+// them into O1 / O2 in place (engine.py:257-277).  Mutation is column-parallel
+// (engine.py:339-373); four warps each run a quarter of every child's pairs.
+struct TileCtx {
+    const hga_run_args* A;
+    RunWs2* ws;
+    const SelView* V;
+    const FeistelKey* fkey;
+    const uint32_t* pop_old;
+    uint32_t* pop_new;
+    int64_t* f_new;
+    int64_t N;
+    int nc, nr;
+    uint64_t gen;
+    int gp, gshift, g;
+};
+
+// Step a: parents by rank (warp 0), crossover points (warp 3), mutation plans (warps 1-3).
+template <int M>
+__device__ __forceinline__ void tile_prepare(const TileCtx& C, TileShared& S, int64_t p0, int cnt, LocalAcc& L) {
     const int t = threadIdx.x & (kR2Threads - 1), k = t >> 5, o = t & 31;
     const int noff = 2 * cnt;
-    const int per_off = nc + 2 * nr;
+    const int per_off = C.nc + 2 * C.nr;
     const int nblk = (per_off + 3) >> 2;
-
-    // a. warp 0: parents (select: slot -> rank -> survivor); warp 3: crossover
-    //    points; warps 1-3: Philox mutation plans
+    const int64_t N = C.N;
     if (k == 0) {
         const bool act = o < noff;
         int64_t f = 0;
         if (act) {
             const int q = o >> 1, b = o & 1;
             const int64_t slot = (int64_t)b * N + p0 + q;
-            const unsigned long long kv = survivor_by_rank(V, feistel2_inv((uint32_t)slot, fkey));
+            const unsigned long long kv = survivor_by_rank(*C.V, feistel2_inv((uint32_t)slot, *C.fkey));
             S.pidx[o] = (int32_t)(kv & 0xffffffffu);
             f = (int64_t)(kv >> 32);
-            f_new[slot] = f;
+            C.f_new[slot] = f;
             const unsigned long long key = ((unsigned long long)f << 32) | (unsigned long long)slot;
             L.best = min(L.best, key);
             L.pbest = min(L.pbest, key);
         }
-        local_hist_add(L, ws, gp ^ 1, act, (uint32_t)(f >> gshift));
+        local_hist_add(L, C.ws, C.gp ^ 1, act, (uint32_t)(f >> C.gshift));
     } else {
         if (k == kTeam - 1 && o < cnt) {
             const int64_t p = p0 + o;
-            const U4 r = draw4(A.seed, (uint32_t)p, (uint32_t)(p >> 32), gen, (uint32_t)kPCrossover);
+            const U4 r = draw4(C.A->seed, (uint32_t)p, (uint32_t)(p >> 32), C.gen, (uint32_t)kPCrossover);
             S.point[o] = (int16_t)(1 + bounded(r.x, (uint32_t)(M - 1)));
         }
         for (int x = t - 32; x < noff * nblk; x += kR2Threads - 32) {
             const int ol = x / nblk, blk = x - (x / nblk) * nblk;
             const int q = ol >> 1;
             int64_t prow = (ol & 1) ? N + p0 + q : p0 + q;  // plan row as engine.py: O1 -> p, O2 -> N + p
-            if (A.strategy == HGA_MUT_SHARED) prow = 0;
-            const U4 r = draw4(A.seed, (uint32_t)prow, (uint32_t)blk | ((uint32_t)(prow >> 32) << 16), gen,
+            if (C.A->strategy == HGA_MUT_SHARED) prow = 0;
+            const U4 r = draw4(C.A->seed, (uint32_t)prow, (uint32_t)blk | ((uint32_t)(prow >> 32) << 16), C.gen,
                                (uint32_t)kPMutCol);
 #pragma unroll
             for (int e4 = 0; e4 < 4; ++e4) {
                 const int e = blk * 4 + e4;
                 if (e < per_off)
-                    S.plan[ol][e] = (int8_t)(e < nc ? 1 + bounded(pick(r, e4), (uint32_t)(M - 1))
-                                                    : bounded(pick(r, e4), (uint32_t)M));
+                    S.plan[ol][e] = (int8_t)(e < C.nc ? 1 + bounded(pick(r, e4), (uint32_t)(M - 1))
+                                                      : bounded(pick(r, e4), (uint32_t)M));
             }
         }
     }
-    if (tm) ts[12] = gtimer();
-    group_sync(g);
-    // b. gather the parents; write them to the new population's parent slots
+}
+
+// Step b: async gather of the 2 cnt parents into rows (one commit group).
+template <int M>
+__device__ __forceinline__ void tile_gather(const TileCtx& C, const TileShared& S, uint4* rows, int cnt) {
+    using G = RunGeom<M>;
+    const int t = threadIdx.x & (kR2Threads - 1);
+    for (int x = t; x < 2 * cnt * G::U; x += kR2Threads) {
+        const int pi = x / G::U, u = x - (x / G::U) * G::U;
+        cp_async16(rows + pi * G::STU + u, reinterpret_cast<const uint4*>(C.pop_old + (int64_t)S.pidx[pi] * G::MW) + u);
+    }
+}
+
+// Steps b'-g on landed rows; ends with a group barrier.
+template <int M, int VM>
+__device__ __forceinline__ void tile_compute(const TileCtx& C, TileShared& S, uint4* rows, int64_t p0, int cnt,
+                                             LocalAcc& L) {
+    using G = RunGeom<M>;
+    constexpr int W = G::W;
+    const int64_t N = C.N;
+    const int t = threadIdx.x & (kR2Threads - 1), k = t >> 5, o = t & 31;
+    const int noff = 2 * cnt;
+    const int nc = C.nc, nr = C.nr;
+    const int g = C.g;
+    // b'. parents to the new population's parent slots (block A, then block B)
     for (int x = t; x < noff * G::U; x += kR2Threads) {
         const int b = x / (cnt * G::U);
         const int r = x - b * cnt * G::U;
         const int q = r / G::U, u = r - q * G::U;
-        const int pi = 2 * q + b;
-        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(pop_old + (int64_t)S.pidx[pi] * G::MW) + u);
-        rows[pi * G::STU + u] = v;
-        reinterpret_cast<uint4*>(pop_new + ((int64_t)b * N + p0 + q) * G::MW)[u] = v;
+        reinterpret_cast<uint4*>(C.pop_new + ((int64_t)b * N + p0 + q) * G::MW)[u] = rows[(2 * q + b) * G::STU + u];
     }
-    if (tm) ts[13] = gtimer();
     group_sync(g);
     // c. column-block crossover in place
     for (int x = t; x < cnt * M; x += kR2Threads) {
@@ -416,7 +439,6 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
             }
         }
     }
-    if (tm) ts[14] = gtimer();
     group_sync(g);
     // d. mutation: thread (k, o) handles plan entries jc = k, k + 4, ...; an
     //    entry whose column already appeared earlier is skipped, and the first
@@ -447,7 +469,6 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
             }
         }
     }
-    if (tm) ts[15] = gtimer();
     group_sync(g);
     // e. pair chain, a quarter per warp
     if (o < noff) {
@@ -472,7 +493,6 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
         S.part[k][2][o] = s.sp;
         S.part[k][3][o] = s.spp;
     }
-    if (tm) ts[16] = gtimer();
     group_sync(g);
     // f. warp 0: children's fitness, best key, next histogram
     if (k == 0) {
@@ -489,21 +509,47 @@ __device__ __forceinline__ void offspring_tile_v4(const hga_run_args& A, RunWs2*
             }
             value = variant_value<M, VM>(s, G::NP);
             const int64_t slot = 2 * N + (int64_t)(o & 1) * N + p0 + (o >> 1);
-            f_new[slot] = value;
+            C.f_new[slot] = value;
             L.best = min(L.best, ((unsigned long long)value << 32) | (unsigned long long)slot);
         }
-        local_hist_add(L, ws, gp ^ 1, active, (uint32_t)(value >> gshift));
+        local_hist_add(L, C.ws, C.gp ^ 1, active, (uint32_t)(value >> C.gshift));
     }
-    if (tm) ts[17] = gtimer();
     // g. coalesced store of the children (O1 block, then O2 block)
     for (int x = t; x < noff * G::U; x += kR2Threads) {
         const int b = x / (cnt * G::U);
         const int r = x - b * cnt * G::U;
         const int q = r / G::U, u = r - q * G::U;
-        reinterpret_cast<uint4*>(pop_new + (2 * N + (int64_t)b * N + p0 + q) * G::MW)[u] = rows[(2 * q + b) * G::STU + u];
+        reinterpret_cast<uint4*>(C.pop_new + (2 * N + (int64_t)b * N + p0 + q) * G::MW)[u] = rows[(2 * q + b) * G::STU + u];
     }
     group_sync(g);
-    if (tm) ts[18] = gtimer();
+}
+
+template <int M, int VM>
+__device__ __forceinline__ void group_tiles(const TileCtx& C, int64_t first, int64_t stride, int64_t ntiles,
+                                            uint4* rows0, uint4* rows1, TileShared* S0, TileShared* S1,
+                                            LocalAcc& L) {
+    if (first >= ntiles) return;
+    const int64_t N = C.N;
+    uint4* rows[2] = {rows0, rows1};
+    TileShared* S[2] = {S0, S1};
+    auto cnt_of = [&](int64_t tile) { return (int)min((int64_t)kR2Pairs, N - tile * kR2Pairs); };
+    tile_prepare<M>(C, *S[0], first * kR2Pairs, cnt_of(first), L);
+    group_sync(C.g);
+    tile_gather<M>(C, *S[0], rows[0], cnt_of(first));
+    cp_async_commit();
+    int cur = 0;
+    for (int64_t tile = first; tile < ntiles; tile += stride) {
+        const int64_t nxt = tile + stride;
+        if (nxt < ntiles) tile_prepare<M>(C, *S[cur ^ 1], nxt * kR2Pairs, cnt_of(nxt), L);
+        group_sync(C.g);
+        if (nxt < ntiles) tile_gather<M>(C, *S[cur ^ 1], rows[cur ^ 1], cnt_of(nxt));
+        cp_async_commit();
+        cp_async_wait<1>();
+        group_sync(C.g);
+        tile_compute<M, VM>(C, *S[cur], rows[cur], tile * kR2Pairs, cnt_of(tile), L);
+        cur ^= 1;
+    }
+    cp_async_wait<0>();
 }
 
 constexpr int kMaxNb = 512;  // prefix scan: one pass of <= 16 warps
@@ -514,7 +560,6 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     __shared__ uint64_t sscr[32];
     __shared__ int s_bin;
     __shared__ uint64_t s_below;
-    __shared__ TileShared S[GROUPS];
     __shared__ uint32_t s_hist[kWin];
     __shared__ uint32_t s_kmin, s_kmax;
     __shared__ unsigned long long s_best, s_pbest;
@@ -538,7 +583,14 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     // warps taking part in the select scans (the rest only meet the barriers)
     const int pw_sel = (int)min((int64_t)nw, (chunk / kSelItems + 31) / 32);
     const int pw_pre = (nb + 31) / 32;  // nb <= kMaxNb = 32 * 32
-    uint4* rows = reinterpret_cast<uint4*>(smem) + (size_t)g * kTileOff * G::STU;
+    // dynamic shared memory: per group, two row buffers and two tile records
+    constexpr size_t kRowsBytes = (size_t)kTileOff * G::STU * 16;
+    constexpr size_t kGroupBytes = 2 * kRowsBytes + 2 * ((sizeof(TileShared) + 15) & ~(size_t)15);
+    unsigned char* gbase = smem + (size_t)g * kGroupBytes;
+    uint4* rows0 = reinterpret_cast<uint4*>(gbase);
+    uint4* rows1 = reinterpret_cast<uint4*>(gbase + kRowsBytes);
+    TileShared* S0 = reinterpret_cast<TileShared*>(gbase + 2 * kRowsBytes);
+    TileShared* S1 = reinterpret_cast<TileShared*>(gbase + 2 * kRowsBytes + ((sizeof(TileShared) + 15) & ~(size_t)15));
 
     int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
     int parity = (int)A.state[3];
@@ -680,13 +732,9 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
         SelView V{s_ltpre, s_eqpre, nb, chunk, lt_list, eq_list, s_ltpre[nb]};
         const FeistelKey fkey = make_feistel_key(draw4(A.seed, 0, 0, (uint64_t)gen, (uint32_t)kPSelect), (uint32_t)half);
         if (timing && gi < 64) ws->tstamp[gi][7] = gtimer();
-        for (int64_t tile = (int64_t)bid * GROUPS + g; tile < ntiles; tile += (int64_t)nb * GROUPS) {
-            const int64_t p0 = tile * kR2Pairs;
-            const int cnt = (int)min((int64_t)kR2Pairs, N - p0);
-            unsigned long long* ts = (A.flags & HGA_RUN_TIMING) != 0 && bid == 0 && g == 0 && gi < 64 &&
-                                             tile == (int64_t)bid * GROUPS + g ? ws->tstamp[gi] : nullptr;
-            offspring_tile_v4<M, VM>(A, ws, V, fkey, pop_old, pop_new, f_old, f_new, p0, cnt, nc, nr, (uint64_t)gen,
-                                     gp, gshift, rows, S[g], L, g, ts);
+        {
+            TileCtx C{&A, ws, &V, &fkey, pop_old, pop_new, f_new, N, nc, nr, (uint64_t)gen, gp, gshift, g};
+            group_tiles<M, VM>(C, (int64_t)bid * GROUPS + g, (int64_t)nb * GROUPS, ntiles, rows0, rows1, S0, S1, L);
         }
         if (timing && gi < 64) ws->tstamp[gi][8] = gtimer();
         // flush the CTA's histogram window, key range and best keys
@@ -855,7 +903,7 @@ int launch_run_v2_mv(const hga_run_args* a, cudaStream_t st) {
     Run2Params P;
     P.a = *a;
     P.gshift = run2_granule_shift(a->fit_var);
-    const int smem = GROUPS * kTileOff * RunGeom<M>::STU * 16;
+    const int smem = GROUPS * (2 * kTileOff * RunGeom<M>::STU * 16 + 2 * (int)((sizeof(TileShared) + 15) & ~(size_t)15));
     auto kern = k_run_v3<M, VM, GROUPS>;
     static bool attr = false;
     if (!attr) {

@@ -37,14 +37,7 @@ for m, N in ((12, 1000), (20, 10_000), (28, 31_250), (36, 312_500)):
     print(json.dumps({"m": m, "detail_us": {"B": med(ts[:, 1] - ts[:, 0]), "bar1": med(ts[:, 2] - ts[:, 1]),
                                              "E_prefix": med(ts[:, 7] - ts[:, 2]), "E_tiles": med(ts[:, 8] - ts[:, 7]),
                                              "E_flush": med(ts[:, 9] - ts[:, 8]), "bar2": med(ts[:, 4] - ts[:, 9]),
-                                             "F": med(ts[1:, 0] - ts[:-1, 4]),
-                                             "tile0": {"a_parents_plans": med(ts[:, 12] - ts[:, 7]),
-                                                       "b_gather": med(ts[:, 13] - ts[:, 12]),
-                                                       "c_crossover": med(ts[:, 14] - ts[:, 13]),
-                                                       "d_mutation": med(ts[:, 15] - ts[:, 14]),
-                                                       "e_pairs": med(ts[:, 16] - ts[:, 15]),
-                                                       "f_finish": med(ts[:, 17] - ts[:, 16]),
-                                                       "g_store": med(ts[:, 18] - ts[:, 17])}},
+                                             "F": med(ts[1:, 0] - ts[:-1, 4])},
                       "sm_mhz": float(np.median((ts[:, 11] - ts[:, 10]) / (ts[:, 4] - ts[:, 0]) * 1e3))}))
     gen = np.diff(ts[:, 0])
     print(json.dumps({"m": m, "N": N, "us_per_gen": float(np.median(gen)) / 1e3,
