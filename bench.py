@@ -239,6 +239,21 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e through the public API with host (numpy) buffers
     e2e = run_e2e(args, cfg, hga, engine, torch)
+    # the same public call on the device-resident SearchState (each step reads
+    # back its trace entry / best fitness): what run_search-style users get
+    st2 = hga.initial_state(cfg)
+    for _ in range(3):
+        hga.step(st2)
+    torch.cuda.synchronize()
+    n_res = max(10, min(args.steps, 200))
+    t0 = time.perf_counter()
+    for _ in range(n_res):
+        hga.step(st2)
+    t_res = (time.perf_counter() - t0) / n_res
+    e2e_resident = {"value": 2 * N_PAIRS / t_res, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 72,
+                    "steps": n_res, "ms_per_step": t_res * 1e3,
+                    "api": "paper_2208_14961_b200.step(state) on the device-resident SearchState (trace entry + "
+                           "8-word state read back every step)"}
 
     # fitness-only sweep (config 5) at large n: the kernel's own roofline
     sweep = run_fitness_sweep(args, engine, torch, lib, peak) if not args.no_sweep else None
@@ -266,6 +281,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": args.steps + (5 * (args.steps // MIGRATE_EVERY) if world > 1 else 0),
         "roofline": roofline,
         "e2e": e2e,
+        "e2e_resident": e2e_resident,
         "persistent_run": {"value": persistent * world, "unit": UNIT, "generations_per_launch": args.steps,
                            "note": "production run_search mode: K generations in one launch, L2 warm"},
         "wall_seconds_timed_region": wall,

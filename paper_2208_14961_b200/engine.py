@@ -463,6 +463,7 @@ class _Resident:
         self.trace_dev = torch.zeros(1024, dtype=torch.int64, device=self.dev)
         self.key = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.run_ws = None
+        self.host_state = None
         self.sel_ws = None
         self.perm_ws = None
 
@@ -627,11 +628,19 @@ def _step_reference(state: SearchState) -> None:
 
 
 def _sync_from_device(state: SearchState) -> None:
-    """Pull the 8-word device state + new trace entries after hga_run."""
+    """Pull the 8-word device state (+ new trace entries) after hga_run: one
+    small pinned D2H when a single generation ran (its trace value is
+    state[7])."""
     res = state._res
-    st = res.dstate.cpu().tolist()
+    if res.host_state is None:
+        res.host_state = torch.empty(8, dtype=torch.int64, pin_memory=True)
+    res.host_state.copy_(res.dstate, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    st = res.host_state.tolist()
     it = int(st[0])
-    if it > state.iteration:
+    if it == state.iteration + 1:
+        state.trace.append(int(st[7]))
+    elif it > state.iteration:
         state.trace.extend(int(v) for v in res.trace_dev[state.iteration + 1:it + 1].cpu().tolist())
     improved = int(st[1]) < state.best_fitness
     state.iteration = it

@@ -336,3 +336,37 @@ def test_single_gpu_island_and_elites(cuda_device):
     isl.advance(2)
     p2 = isl.state.population
     assert np.array_equal(isl.state.fitness, oracle.evaluate(p2, "f2"))
+
+
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=60, deadline=None)
+@given(m=st.integers(1, 70), n=st.integers(1, 300), seed=st.integers(0, 2**31), balanced=st.booleans())
+def test_fitness_fuzz_vs_oracle(m, n, seed, balanced):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if balanced and m % 4 == 0:
+        pop = oracle.random_balanced(m, n, seed, 1, 0, 0)
+    else:
+        pop = np.random.default_rng(seed).choice(np.array([-1, 1], dtype=np.int8), size=(n, m, m))
+    want = oracle.penalties(pop, threads=2)
+    got = hga.penalties(pop)
+    for col, key in enumerate(("f1", "f2", "orth", "sq")):
+        assert np.array_equal(got[key], want[:, col]), (m, key)
+
+
+@pytest.mark.parametrize("total,k", [(10, 1), (4000, 7), (40_000, 16), (40_000, 20_000), (123_457, 999)])
+def test_select_smallest_is_stable_topk(total, k, cuda_device):
+    rng = np.random.default_rng(total + k)
+    fit = rng.integers(0, 64, size=total).astype(np.int64) * 2
+    t = torch.from_numpy(fit).cuda()
+    out = torch.empty(k, dtype=torch.int64, device="cuda")
+    wsb = int(hga._lib.lib.hga_select_ws_bytes(total))
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rc = hga._lib.lib.hga_select_smallest(t.data_ptr(), total, k, out.data_ptr(), flag.data_ptr(), ws.data_ptr(), wsb,
+                                          torch.cuda.current_stream().cuda_stream)
+    assert rc == 0 and int(flag.item()) == 0
+    assert np.array_equal(out.cpu().numpy(), np.argsort(fit, kind="stable")[:k])
