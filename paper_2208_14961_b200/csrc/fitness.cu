@@ -98,11 +98,11 @@ __global__ void __launch_bounds__(kFitThreads)
         Col<W> c;
         if (FROM_I8) {
             bad |= stage_bytes(reinterpret_cast<const int8_t*>(src) + k0 * mm, sraw, cnt * mm);
-            if (tid < cnt * 3) sacc[tid] = 0;
+            for (int z = tid; z < cnt * 3; z += blockDim.x) sacc[z] = 0;
             __syncthreads();
             if (active) pack_column_smem<W>(sraw + kl * mm, m, i, c);
         } else {
-            if (tid < cnt * 3) sacc[tid] = 0;
+            for (int z = tid; z < cnt * 3; z += blockDim.x) sacc[z] = 0;
             if (active) {
                 const uint32_t* g = reinterpret_cast<const uint32_t*>(src) + (k0 + kl) * mw + (int64_t)i * W;
 #pragma unroll
