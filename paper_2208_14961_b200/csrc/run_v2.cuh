@@ -598,6 +598,8 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     const bool force = (A.flags & HGA_RUN_FORCE) != 0;
     bool stop = !force && A.state[5] != 0;
     const bool timing = (A.flags & HGA_RUN_TIMING) != 0 && bid == 0 && tid == 0;
+    uint32_t next_kmin = 0, next_kmax = 0;
+    bool have_krange = false;
 
     for (int64_t gi = 0; gi < A.gens_this_call && !stop; ++gi) {
         const int64_t gen = iter + 1;
@@ -615,7 +617,11 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
         // first batch of fitness values: independent of tau, so load it under the histogram scan
         int64_t fpre[kSelItems];
         if (wid < pw_sel) load_items(f_old, lo + (int64_t)tid * kSelItems, hi, fpre);
-        const uint32_t kmin = __ldcg(&ws->kmin[gp]), kmax = __ldcg(&ws->kmax[gp]);
+        if (!have_krange) {  // otherwise read with the bookkeeping loads of the previous generation
+            next_kmin = __ldcg(&ws->kmin[gp]);
+            next_kmax = __ldcg(&ws->kmax[gp]);
+        }
+        const uint32_t kmin = next_kmin, kmax = next_kmax;
         if (wid == 0) kth_bin_warp(&ws->hist[gp][kmin], (int)(kmax - kmin + 1), (uint64_t)half, &s_bin, &s_below);
         __syncthreads();
         const int64_t tau = (int64_t)(kmin + (uint32_t)s_bin) << gshift;
@@ -772,6 +778,9 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
         // ---- F: bookkeeping (identical in every CTA)
         {
             const unsigned long long key = __ldcg(&ws->best_key[gp]);
+            next_kmin = __ldcg(&ws->kmin[gp ^ 1]);  // key range of the next generation's histogram
+            next_kmax = __ldcg(&ws->kmax[gp ^ 1]);
+            have_krange = true;
             const int64_t v = (int64_t)(key >> 32);
             const int64_t idx = (int64_t)(key & 0xffffffffu);
             iter = gen;
@@ -866,6 +875,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
                 grid_sync(&ws->bar);
                 if (bid == 0 && tid == 0) ws->restart_key = ~0ull;
                 stop = best == 0;
+                have_krange = false;  // the histogram was rebuilt
             }
         }
     }
