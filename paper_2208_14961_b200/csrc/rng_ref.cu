@@ -4,8 +4,9 @@
 //
 // Every draw is a pure function of (seed, stream id, counter): one thread per
 // draw.  The only sequential piece is Fisher-Yates (rand.py:131-140); its swap
-// targets are drawn in parallel and the swap chain runs in one CTA, in shared
-// memory when the permutation fits.
+// targets are drawn in parallel, then small permutations run the swap chain in
+// one CTA's shared memory and large ones are replayed in parallel (k_pfy_*:
+// grouping the steps by target turns the chain into short pointer chases).
 #include "hga_common.cuh"
 
 namespace hga {
@@ -47,6 +48,111 @@ __global__ void k_perm_chain(const int32_t* __restrict__ b, int64_t n, int64_t* 
     }
     __syncthreads();
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = perm[i];
+}
+
+// ---------------------------------------------------------------------
+// Parallel replay of the same forward Fisher-Yates (rand.py:131-140) for
+// large n.  With b[a] >= a the partner of step a, position a is final after
+// step a, so:
+//   v[a]     = value at position a just before step a
+//            = v[k] for the last k < a with b[k] == a, else a      (a chain)
+//   final[a] = v[k] for the last k < a with b[k] == b[a], else b[a]
+//   final[n-1] = v[n-1]
+// Steps are grouped by target (counting sort, then each small group sorted
+// by step index), which gives both "last k" lookups; v follows the chains.
+__global__ void k_pfy_targets(uint64_t key, uint64_t c0, int64_t n, int32_t* b, int32_t* cnt) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a + 1 < n;
+         a += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t t = (int32_t)(a + (int64_t)(stream_word(key, c0 + (uint64_t)a) % (uint64_t)(n - a)));
+        b[a] = t;
+        atomicAdd(&cnt[t], 1);
+    }
+}
+
+// single CTA: exclusive scan of cnt[0..n) into off[0..n]
+__global__ void __launch_bounds__(1024) k_pfy_scan(const int32_t* __restrict__ cnt, int64_t n, int32_t* off) {
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t carry;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < n; b0 += 1024) {
+        const int64_t i = b0 + tid;
+        const int32_t v = i < n ? cnt[i] : 0;
+        int32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int32_t t = wsum[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            wsum[lane] = t;
+        }
+        __syncthreads();
+        if (i < n) off[i] = carry + (wid ? wsum[wid - 1] : 0) + x - v;
+        __syncthreads();
+        if (tid == 0) carry += wsum[31];
+        __syncthreads();
+    }
+    if (tid == 0) off[n] = carry;
+}
+
+__global__ void k_pfy_place(const int32_t* __restrict__ b, int64_t n, int32_t* cursor, int32_t* grouped) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a + 1 < n;
+         a += (int64_t)gridDim.x * blockDim.x)
+        grouped[atomicAdd(&cursor[b[a]], 1)] = (int32_t)a;
+}
+
+// one thread per target y: sort its (few) steps, emit prev_same and last_hit
+__global__ void k_pfy_groups(const int32_t* __restrict__ off, int64_t n, int32_t* grouped, int32_t* prev_same,
+                             int32_t* last_hit) {
+    for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y < n; y += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s0 = off[y], s1 = off[y + 1];
+        for (int32_t i = s0 + 1; i < s1; ++i) {  // insertion sort by step index
+            const int32_t v = grouped[i];
+            int32_t j = i - 1;
+            while (j >= s0 && grouped[j] > v) {
+                grouped[j + 1] = grouped[j];
+                --j;
+            }
+            grouped[j + 1] = v;
+        }
+        int32_t lh = -1, prev = -1;
+        for (int32_t i = s0; i < s1; ++i) {
+            const int32_t k = grouped[i];
+            prev_same[k] = prev;
+            prev = k;
+            if (k < y) lh = k;
+        }
+        last_hit[y] = lh;
+    }
+}
+
+__global__ void k_pfy_final(const int32_t* __restrict__ b, const int32_t* __restrict__ prev_same,
+                            const int32_t* __restrict__ last_hit, int64_t n, int64_t* out) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x) {
+        int32_t src;
+        if (a + 1 < n) {
+            const int32_t k = prev_same[a];
+            if (k < 0) {
+                out[a] = b[a];
+                continue;
+            }
+            src = k;
+        } else {
+            src = (int32_t)a;
+        }
+        // v[src]: follow last_hit to the chain's root
+        int32_t x = src;
+        while (last_hit[x] >= 0) x = last_hit[x];
+        out[a] = x;
+    }
 }
 
 // engine._random_balanced: column c of slot s starts with rows [0, m/2) = -1
@@ -156,10 +262,12 @@ int hga_ref_uniform(uint64_t seed, uint64_t stream_id, uint64_t counter0, int64_
     return to_rc(cudaGetLastError());
 }
 
+constexpr int64_t kPermParallelMin = 8192;  // above this the parallel replay wins
+
 size_t hga_ref_permutation_ws_bytes(int64_t n) {
     if (n <= 0) return 0;
-    size_t b = (size_t)n * 4;
-    if (n > kPermSmemMax) b += (size_t)n * 4;
+    size_t b = (n >= kPermParallelMin) ? (size_t)(7 * n + 8) * 4 : (size_t)n * 4;
+    if (n > kPermSmemMax && n < kPermParallelMin) b += (size_t)n * 4;
     return (b + 255) & ~(size_t)255;
 }
 
@@ -169,6 +277,25 @@ int hga_ref_permutation(uint64_t seed, uint64_t stream_id, uint64_t counter0, in
     if (ws_bytes < hga_ref_permutation_ws_bytes(n) || !ws) return HGA_E_WORKSPACE;
     cudaStream_t st = (cudaStream_t)stream;
     int32_t* b = (int32_t*)ws;
+    if (n >= kPermParallelMin) {
+        int32_t* cnt = b + n;
+        int32_t* off = cnt + n;        // n + 1
+        int32_t* cursor = off + n + 1;
+        int32_t* grouped = cursor + n;
+        int32_t* prev_same = grouped + n;
+        int32_t* last_hit = prev_same + n;
+        cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)n * 4, st);
+        if (e != cudaSuccess) return to_rc(e);
+        const uint64_t key = stream_key(seed, stream_id);
+        k_pfy_targets<<<grid1d(n), 256, 0, st>>>(key, counter0, n, b, cnt);
+        k_pfy_scan<<<1, 1024, 0, st>>>(cnt, n, off);
+        e = cudaMemcpyAsync(cursor, off, (size_t)n * 4, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return to_rc(e);
+        k_pfy_place<<<grid1d(n), 256, 0, st>>>(b, n, cursor, grouped);
+        k_pfy_groups<<<grid1d(n), 256, 0, st>>>(off, n, grouped, prev_same, last_hit);
+        k_pfy_final<<<grid1d(n), 256, 0, st>>>(b, prev_same, last_hit, n, out);
+        return to_rc(cudaGetLastError());
+    }
     int32_t* gperm = b + n;
     if (n > 1)
         k_perm_targets<<<grid1d(n), 256, 0, st>>>(stream_key(seed, stream_id), counter0, n, b);
