@@ -651,11 +651,15 @@ def _sync_from_device(state: SearchState) -> None:
         state.best_matrix = _best_from_packed(res, res.best_packed)
 
 
-def _run_device(state: SearchState, gens: int) -> None:
+def _run_device(state: SearchState, gens: int, force: bool = False) -> None:
+    """`gens` generations in one persistent launch; `force` runs all of them
+    even past a solution (the reference bench's fixed-length legs)."""
     res = state._res
     res.ensure_trace(state.iteration + gens)
     a = res.run_args()
     a.gens_this_call = gens
+    if force:
+        a.flags = RUN_FORCE
     check(lib.hga_run(a, stream_ptr()), "hga_run")
     _sync_from_device(state)
 
