@@ -77,7 +77,10 @@ int hga_sm_count(int device);
  * NULL; `variants` selects which are computed (fused in one pass, the Gram
  * matrix never leaves the SM).  bad_flag (nullable) gets HGA_FLAG_NOT_SIGN
  * OR-ed in when an entry is not +-1.  ws is needed only for m > 128
- * (hga_fitness_i8_ws_bytes). */
+ * (hga_fitness_i8_ws_bytes).  Orders 36..64 (16-byte aligned pop) run the
+ * Gram on the tensor cores (tcgen05.mma.kind::i8, accumulators in TMEM);
+ * the others, or HGA_FITNESS_TC=0 in the environment, the XOR+POPC kernels.
+ * Results are identical. */
 size_t hga_fitness_i8_ws_bytes(int64_t n, int32_t m);
 int hga_fitness_i8(const int8_t *pop, int64_t n, int32_t m, uint32_t variants, int64_t *f1,
                    int64_t *f2, int64_t *orth, int64_t *sq, int32_t *bad_flag, void *ws,
@@ -193,6 +196,15 @@ typedef struct hga_run_args {
 
 #define HGA_RUN_FORCE 1u
 #define HGA_RUN_TIMING 2u  /* record per-phase %globaltimer stamps (diagnostics) */
+/* Select survivors with the one-barrier generation loop (4N <= 131072):
+ * every CTA reads all 16-bit selection keys after the barrier instead of
+ * publishing survivor lists behind a second barrier.  Same survivors, same
+ * ranks, identical runs; measured slower than the default two-barrier loop
+ * on B200 (22.8 vs 17.2 us per generation at order 20, 4N = 40,000), kept for
+ * experiments.  Must be the same on hga_run_init / hga_run_prepare and on
+ * every hga_run of that state (the loops keep selection state in different
+ * slots). */
+#define HGA_RUN_ONE_BARRIER 4u
 
 /* Philox balanced matrices into slots [first_slot, first_slot + count) of
  * the packed population `cols` (slot 0 at cols).  The production-mode

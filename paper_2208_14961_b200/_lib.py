@@ -28,6 +28,7 @@ FLAG_NOT_SIGN, FLAG_POINT_RANGE, FLAG_PLAN_RANGE, FLAG_FIT_RANGE = 1, 2, 4, 8
 
 RUN_FORCE = 1
 RUN_TIMING = 2
+RUN_ONE_BARRIER = 4  # HGA_RUN_ONE_BARRIER: opt-in one-barrier generation loop (identical runs)
 
 MUT_CODES = {"shared": 0, "per-matrix": 1, "multi": 2}
 

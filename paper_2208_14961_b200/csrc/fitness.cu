@@ -14,9 +14,24 @@
 // +-1 on the way), then each thread packs its own column from shared memory.
 #include "fitness_v2.cuh"
 
+#include <cstdlib>
+
 namespace hga {
 
 HGA_V2_ORDERS(HGA_V2_EXTERN)
+
+// tensor-core int8 path (fitness_tc.cu), orders 36..64
+bool fit_tc_order(int m, bool all);
+int launch_fit_tc(int m, const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth,
+                  int64_t* sq, int32_t* bad, cudaStream_t st);
+// HGA_FITNESS_TC=0 selects the XOR+POPC kernels at every order, =all the
+// tensor cores at every order 4..64 (cross-checks, A/B timing)
+static int fit_tc_mode() {
+    const char* e = std::getenv("HGA_FITNESS_TC");
+    if (e && e[0] == '0') return 0;
+    if (e && e[0] == 'a') return 2;
+    return 1;
+}
 
 static int launch_fit_v2(int m, bool from_i8, const void* src, int64_t n, uint32_t v, int64_t* f1, int64_t* f2,
                          int64_t* orth, int64_t* sq, int32_t* bad, cudaStream_t st) {
@@ -323,6 +338,9 @@ int hga_fitness_i8(const int8_t* pop, int64_t n, int32_t m, uint32_t variants, i
     if (n < 0 || m < 1 || m > 4096 || (variants & ~HGA_VAR_ALL) || !variants) return HGA_E_INVALID;
     if (n == 0) return HGA_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    const int tc_mode = fit_tc_mode();
+    if (tc_mode && fit_tc_order(m, tc_mode == 2) && (((uintptr_t)pop) & 15) == 0)
+        return launch_fit_tc(m, pop, n, variants, f1, f2, orth, sq, bad_flag, st);
     if (v2_order(m) && (((uintptr_t)pop) & 15) == 0)
         return launch_fit_v2(m, true, pop, n, variants, f1, f2, orth, sq, bad_flag, st);
     if (m <= 32 * kMaxRegWords)

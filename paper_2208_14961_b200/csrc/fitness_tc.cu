@@ -1,0 +1,419 @@
+// fitness_tc.cu -- int8 fitness on the 5th-generation tensor cores for
+// orders m = 4..64 (engine._fitness_batch, reference engine.py:200-213).
+//
+// The reference forms the column Gram G = Q^T Q of every matrix with a
+// batched float32 matmul and reduces it to F1 = sum|G| - m^2 / F2 = nnz(G) - m.
+// Here G comes from tcgen05.mma.kind::i8 (s8 x s8 -> s32, exact), straight
+// from the reference's int8 bytes:
+//
+//   * Q (row-major, r = K index, c = MN index) is read as an MN-major
+//     operand; A and B are the SAME shared-memory tile.  Loader warps move
+//     the matrix bytes with cp.async (16/8/4-byte pieces, the widest the
+//     order's row pitch allows) straight into the canonical no-swizzle
+//     layout: 16-column groups of KP (= 64) rows x 16 bytes, core matrices
+//     of 8 rows contiguous (LBO = 128 B between K groups, SBO = KP*16 B
+//     between column groups).  Padding (rows >= m, columns >= m, the fourth
+//     column group at m <= 48) is never written and stays zero, so padded
+//     Gram entries are exactly 0.
+//   * Two matrices per MMA pair: M = 64 MMAs (K = 32 per instruction, two
+//     K steps) whose accumulators interleave in TMEM (the second at lane
+//     offset 16), so each of the four epilogue warps (one per TMEM lane
+//     quarter) gets 16 Gram rows of each matrix: the work is balanced for
+//     every order.  Eight accumulator slots (512 TMEM columns) and sixteen
+//     shared-memory stages keep loads, MMAs and epilogues overlapped.
+//   * Epilogue: tcgen05.ld 32x32b.x16 -> registers; each lane sums |g|,
+//     [g != 0] and g^2 over its row; 16-lane shuffles and a 4-warp combine
+//     give the matrix totals.  The same warps check the staged bytes are
+//     +-1 (the v2 kernels' contract: HGA_FLAG_NOT_SIGN otherwise).
+//
+// Roofline: HBM (m^2 + 8 bytes per matrix).  Per matrix the tensor pipe
+// does 2 * 64 * N * 64 MACs (N = 16 ceil(m/16)) and the epilogue ~2 * 64 * N
+// integer ops, both far below the HBM time at these orders.
+#include <cstdint>
+
+#include "hga_common.cuh"
+
+namespace hga {
+namespace tc {
+
+constexpr int kStageBytes = 192 * 1024;  // all stages; > 114 KB keeps one CTA (and one TMEM owner) per SM
+constexpr int kMaxStages = 48;
+constexpr int kB = 2;          // MMA pairs per pipeline unit (one barrier round trip per unit)
+constexpr int kSlotCols = kB * 64;
+constexpr int kSlots = 512 / kSlotCols;  // TMEM accumulator slots
+constexpr int kEpiGroups = 3;  // epilogue groups of 4 warps (one per TMEM lane quarter); group g takes pairs it = g mod 3
+constexpr int kEpiWarps = 4 * kEpiGroups;
+constexpr int kLoadWarps = 4;  // two per tile of the pair
+constexpr int kCheckWarps = kLoadWarps;  // check warp w re-reads what loader warp w copied
+constexpr int kThreads = (kEpiWarps + kLoadWarps + kCheckWarps + 1) * 32;
+constexpr int kMmaWarp = kEpiWarps + kLoadWarps + kCheckWarps;
+
+// A tile is the M = 64 MMA operand: 4 column groups of 16.  Orders <= 16 put
+// four matrices side by side in it (P = 4), orders 17..32 two (P = 2), larger
+// orders one (zero-padded).  With P > 1 the MMA also forms the cross-matrix
+// blocks; the epilogue reads only each matrix's own diagonal block.
+template <int M>
+struct Geo {
+    static_assert(M >= 4 && M <= 64 && M % 4 == 0, "tensor-core path covers orders 4..64");
+    static constexpr int KP = M <= 32 ? 32 : 64;        // padded K (rows)
+    static constexpr int NCG = (M + 15) / 16;           // column groups per matrix
+    static constexpr int P = M <= 16 ? 4 : (M <= 32 ? 2 : 1);  // matrices per tile
+    static constexpr int MPP = 2 * P;                   // matrices per MMA pair (two tiles)
+    static constexpr int N = P > 1 ? 64 : 16 * NCG;     // MMA N
+    static constexpr int COLS = 16 * NCG;               // Gram columns read per lane
+    static constexpr int QPM = P > 1 ? NCG : 4;         // TMEM lane quarters summed per matrix
+    static constexpr int TILE = 4 * KP * 16;
+    static constexpr int GR = (M % 16 == 0) ? 16 : ((M % 8 == 0) ? 8 : 4);  // cp.async piece
+    static constexpr int NG = M * M / GR;               // pieces per matrix
+    static constexpr int PER = (P * NG + 64 - 1) / 64;  // pieces per lane (two loader warps per tile)
+    static constexpr int SBO = KP * 16;
+    static constexpr int STAGES = kStageBytes / (2 * kB * TILE);  // 12 (KP = 64) or 24 (KP = 32)
+    static constexpr uint32_t IDESC = (2u << 4)          // D: s32
+                                      | (1u << 7) | (1u << 10)   // A, B: signed 8-bit
+                                      | (1u << 15) | (1u << 16)  // A, B: MN-major
+                                      | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(64 >> 4) << 24);
+};
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(saddr(b)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void cp_async_piece4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_piece8(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_piece16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// Shared-memory matrix descriptor, no swizzle, MN-major canonical layout.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+           (1ull << 46);  // descriptor version 1 (sm_100); base offset 0, layout SWIZZLE_NONE
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(b))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
+template <int M, int VM>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_fit_i8_tc(const int8_t* __restrict__ pop, int64_t n, uint32_t vm_out, int64_t* __restrict__ f1,
+                int64_t* __restrict__ f2, int64_t* __restrict__ orth, int64_t* __restrict__ sq, int32_t* bad_flag) {
+    using G = Geo<M>;
+    constexpr int UT = 2 * kB;  // tiles per pipeline unit
+    extern __shared__ __align__(1024) uint8_t smem[];  // G::STAGES x UT x G::TILE
+    __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[kSlots], tempty[kSlots];
+    __shared__ uint32_t tmem_base;
+    __shared__ uint32_t part[kEpiGroups][2][kB][2][4][3];  // [group][iteration parity][pair][tile][quarter][sum]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nunits = (n + kB * G::MPP - 1) / (kB * G::MPP);
+
+    // zero the stages once: padding bytes are never written again
+    for (int i = tid; i < G::STAGES * UT * G::TILE / 16; i += kThreads)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid == 0) {
+        for (int s = 0; s < G::STAGES; ++s) {
+            mbar_init(&full[s], kLoadWarps * 32);   // one asynchronous cp.async arrival per loader lane
+            mbar_init(&empty[s], 1 + kCheckWarps);  // MMA commit + the check warps
+        }
+        for (int a = 0; a < kSlots; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeroed stages -> async proxy (MMA reads)
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_base)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tbase = tmem_base;
+    const uint32_t sbase = saddr(smem);
+
+    if (warp >= kEpiWarps && warp < kMmaWarp) {
+        // ------------------------------------------------------------ loaders / byte checkers
+        const bool checker = warp >= kEpiWarps + kLoadWarps;
+        const int lw = (warp - kEpiWarps) % kLoadWarps, j = lw & 1, half = lw >> 1;
+        // per-lane piece table: (source byte offset) | (tile byte offset << 16)
+        uint32_t tab[G::PER];
+#pragma unroll
+        for (int i = 0; i < G::PER; ++i) {
+            const int g = (i * 2 + half) * 32 + lane;  // piece of the tile's P consecutive matrices
+            const int src = g * G::GR;
+            const int e = src / (M * M), o = src - e * (M * M);
+            const int r = o / M, c = o - (o / M) * M;
+            const int dst = e * G::NCG * G::SBO + (c >> 4) * G::SBO + (r >> 3) * 128 + (r & 7) * 16 + (c & 15);
+            tab[i] = g < G::P * G::NG ? ((uint32_t)src | ((uint32_t)dst << 16)) : 0xFFFFFFFFu;
+        }
+        uint32_t bad = 0;
+        int it = 0;
+        for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+            const int s = it % G::STAGES;
+            if (checker) {
+                // +-1 check of the bytes loader warp lw copied, as soon as they have landed
+                mbar_wait(&full[s], (it / G::STAGES) & 1);
+#pragma unroll
+                for (int b = 0; b < kB; ++b) {
+                    const int64_t k0 = (int64_t)G::MPP * (kB * u + b) + (int64_t)G::P * j;
+                    const uint32_t lim = k0 < n ? (uint32_t)min((int64_t)G::P, n - k0) * (uint32_t)(M * M) : 0u;
+                    const uint8_t* tile = smem + (size_t)(s * UT + 2 * b + j) * G::TILE;
+#pragma unroll
+                    for (int i = 0; i < G::PER; ++i) {
+                        if (tab[i] == 0xFFFFFFFFu || (tab[i] & 0xFFFFu) >= lim) continue;
+                        const uint8_t* q8 = tile + (tab[i] >> 16);
+                        uint32_t w[G::GR / 4];
+                        if constexpr (G::GR == 16) {
+                            const uint4 x = *reinterpret_cast<const uint4*>(q8);
+                            w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+                        } else if constexpr (G::GR == 8) {
+                            const uint2 x = *reinterpret_cast<const uint2*>(q8);
+                            w[0] = x.x; w[1] = x.y;
+                        } else {
+                            w[0] = *reinterpret_cast<const uint32_t*>(q8);
+                        }
+#pragma unroll
+                        for (int v4 = 0; v4 < G::GR / 4; ++v4) {
+                            // byte in {0x01, 0xFF}  <=>  a = byte ^ 1 has bit 0 clear and bits 1..7 equal
+                            const uint32_t a8 = w[v4] ^ 0x01010101u, b8 = a8 & 0xFEFEFEFEu;
+                            bad |= (a8 & 0x01010101u) | ((b8 ^ (b8 << 1)) & 0xFCFCFCFCu);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                continue;
+            }
+            mbar_wait(&empty[s], ((it / G::STAGES) & 1) ^ 1);
+#pragma unroll
+            for (int b = 0; b < kB; ++b) {
+                const int64_t k0 = (int64_t)G::MPP * (kB * u + b) + (int64_t)G::P * j;
+                if (k0 >= n) continue;
+                const int8_t* src = pop + k0 * (int64_t)(M * M);
+                const uint32_t lim = (uint32_t)min((int64_t)G::P, n - k0) * (uint32_t)(M * M);
+                const uint32_t dst = sbase + (uint32_t)((s * UT + 2 * b + j) * G::TILE);
+#pragma unroll
+                for (int i = 0; i < G::PER; ++i) {
+                    if (tab[i] != 0xFFFFFFFFu && (tab[i] & 0xFFFFu) < lim) {
+                        const void* gp = src + (tab[i] & 0xFFFFu);
+                        const uint32_t sp = dst + (tab[i] >> 16);
+                        if constexpr (G::GR == 16) cp_async_piece16(sp, gp);
+                        else if constexpr (G::GR == 8) cp_async_piece8(sp, gp);
+                        else cp_async_piece4(sp, gp);
+                    }
+                }
+            }
+            // arrives on full[s] once this lane's copies above have landed (no blocking wait:
+            // up to STAGES units stay in flight per CTA)
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(saddr(&full[s])) : "memory");
+        }
+        if (bad && bad_flag) atomicOr(bad_flag, HGA_FLAG_NOT_SIGN);
+    } else if (warp == kMmaWarp) {
+        // ------------------------------------------------------------ MMA issuer
+        int it = 0;
+        for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
+            const int s = it % G::STAGES, a = it % kSlots;
+            mbar_wait(&full[s], (it / G::STAGES) & 1);
+            mbar_wait(&tempty[a], ((it / kSlots) & 1) ^ 1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> MMA operand reads
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lane == 0) {
+#pragma unroll
+                for (int t = 0; t < UT; ++t) {  // tile t = pair t/2, interleave t%2
+                    const uint32_t tile = sbase + (uint32_t)((s * UT + t) * G::TILE);
+                    const uint32_t d =
+                        tbase + (uint32_t)(a * kSlotCols + (t >> 1) * 64) + ((uint32_t)(16 * (t & 1)) << 16);
+#pragma unroll
+                    for (int ks = 0; ks < G::KP / 32; ++ks) {
+                        const uint64_t desc = sdesc(tile + (uint32_t)(ks * 512), 128u, (uint32_t)G::SBO);
+                        mma_i8(d, desc, desc, G::IDESC, ks > 0 ? 1u : 0u);
+                    }
+                }
+                mma_commit(&empty[s]);
+                mma_commit(&tfull[a]);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 0 .. kEpiWarps-1)
+        // Several groups so that each SM sub-partition has kEpiGroups epilogue
+        // warps to interleave (one warp alone is latency-bound on the reductions).
+        const int q = warp & 3, grp = warp >> 2;  // TMEM lane quarter, epilogue group
+        const int jj = lane >> 4;
+        // Gram symmetry: quarter q holds rows 16 lq .. 16 lq + 15 of its matrix
+        // (lq = local quarter); it reads only column blocks cb >= lq and counts
+        // the off-diagonal blocks twice.
+        const int lq = G::P > 1 ? q % G::NCG : q;
+        const int cs = G::P > 1 ? G::COLS * (q / G::NCG) : 0;  // this quarter's matrix block
+        for (int it = grp;; it += kEpiGroups) {
+            const int64_t u = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+            if (u >= nunits) break;
+            const int a = it % kSlots;
+            mbar_wait(&tfull[a], (it / kSlots) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t(&pp)[kB][2][4][3] = part[grp][(it / kEpiGroups) & 1];
+#pragma unroll
+            for (int b = 0; b < kB; ++b) {
+                uint32_t v[G::NCG][16];
+                const uint32_t taddr = tbase + (uint32_t)(a * kSlotCols + b * 64 + cs) + ((uint32_t)(32 * q) << 16);
+#pragma unroll
+                for (int cb = 0; cb < G::NCG; ++cb)
+                    if (cb >= lq) tmem_ld16(taddr + (uint32_t)(16 * cb), v[cb]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                // weighted row sums over the upper-triangle blocks (padded entries are 0)
+                uint32_t pa[4] = {0, 0, 0, 0}, pn[4] = {0, 0, 0, 0}, ps[4] = {0, 0, 0, 0};  // 4 chains for ILP
+#pragma unroll
+                for (int cb = 0; cb < G::NCG; ++cb) {
+                    if (cb < lq) continue;
+                    const uint32_t wgt = cb == lq ? 1u : 2u;
+                    uint32_t ba[4] = {0, 0, 0, 0}, bn[4] = {0, 0, 0, 0}, bs[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int g = (int)v[cb][e];
+                        if constexpr ((VM & HGA_VAR_F1) != 0) ba[e & 3] += (uint32_t)abs(g);
+                        if constexpr ((VM & (HGA_VAR_F2 | HGA_VAR_ORTH)) != 0) bn[e & 3] += (g != 0);
+                        if constexpr ((VM & HGA_VAR_SQ) != 0) bs[e & 3] += (uint32_t)(g * g);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        pa[c] += wgt * ba[c];
+                        pn[c] += wgt * bn[c];
+                        ps[c] += wgt * bs[c];
+                    }
+                }
+                uint32_t s_abs = (pa[0] + pa[1]) + (pa[2] + pa[3]);
+                uint32_t s_nz = (pn[0] + pn[1]) + (pn[2] + pn[3]);
+                uint32_t s_sq = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+#pragma unroll
+                for (int o = 8; o; o >>= 1) {
+                    s_abs += __shfl_xor_sync(0xffffffffu, s_abs, o);
+                    s_nz += __shfl_xor_sync(0xffffffffu, s_nz, o);
+                    s_sq += __shfl_xor_sync(0xffffffffu, s_sq, o);
+                }
+                if ((lane & 15) == 0) {
+                    pp[b][jj][q][0] = s_abs;
+                    pp[b][jj][q][1] = s_nz;
+                    pp[b][jj][q][2] = s_sq;
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");  // the group's 4 warps
+            if (q == 3 && lane < kB * G::MPP) {  // quarter 3 reads the fewest blocks: it finalises
+                const int b = lane / G::MPP, ml = lane - b * G::MPP;
+                const int64_t k = (int64_t)G::MPP * (kB * u + b) + ml;
+                if (k < n) {
+                    const int jm = ml / G::P, q0 = G::P > 1 ? (ml % G::P) * G::NCG : 0;
+                    uint32_t ta = 0, tn = 0, ts = 0;
+#pragma unroll
+                    for (int w = 0; w < G::QPM; ++w) {
+                        ta += pp[b][jm][q0 + w][0];
+                        tn += pp[b][jm][q0 + w][1];
+                        ts += pp[b][jm][q0 + w][2];
+                    }
+                    // diagonal: g_ii = m for +-1 entries (checked by the check warps)
+                    const int64_t nz_off = (int64_t)tn - M;
+                    if ((vm_out & HGA_VAR_F1) && f1) f1[k] = (int64_t)ta - (int64_t)M * M;
+                    if ((vm_out & HGA_VAR_F2) && f2) f2[k] = nz_off;
+                    if ((vm_out & HGA_VAR_ORTH) && orth) orth[k] = ((int64_t)M * (M - 1) - nz_off) / 2;
+                    if ((vm_out & HGA_VAR_SQ) && sq) sq[k] = (int64_t)ts - (int64_t)M * M * M;
+                }
+            }
+        }
+    }
+
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512) : "memory");
+}
+
+template <int M, int VM>
+static int launch_tc(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth, int64_t* sq,
+                     int32_t* bad, cudaStream_t st) {
+    auto kern = k_fit_i8_tc<M, VM>;
+    constexpr int smem = Geo<M>::STAGES * 2 * kB * Geo<M>::TILE;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return to_rc(e);
+        attr = true;
+    }
+    const int64_t nunits = (n + kB * Geo<M>::MPP - 1) / (kB * Geo<M>::MPP);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nunits, sm_count_cached()));
+    kern<<<grid, kThreads, smem, st>>>(pop, n, v, f1, f2, orth, sq, bad);
+    return to_rc(cudaGetLastError());
+}
+
+template <int M>
+static int launch_tc_m(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth,
+                       int64_t* sq, int32_t* bad, cudaStream_t st) {
+    if ((v & ~(HGA_VAR_F2 | HGA_VAR_ORTH)) == 0)
+        return launch_tc<M, HGA_VAR_F2 | HGA_VAR_ORTH>(pop, n, v, f1, f2, orth, sq, bad, st);
+    if (v == HGA_VAR_F1) return launch_tc<M, HGA_VAR_F1>(pop, n, v, f1, f2, orth, sq, bad, st);
+    return launch_tc<M, HGA_VAR_ALL>(pop, n, v, f1, f2, orth, sq, bad, st);
+}
+
+}  // namespace tc
+
+// Orders routed to the tensor cores by default: measured faster than the
+// XOR+POPC kernels from m = 44 on (B200, 2.5e5 matrices: m = 48 8.0e8 vs
+// 5.9e8 evals/s, m = 64 5.1e8 vs 3.3e8); HGA_FITNESS_TC=all routes every
+// order 4..64, HGA_FITNESS_TC=0 none.
+bool fit_tc_order(int m, bool all) { return (m % 4) == 0 && m >= (all ? 4 : 44) && m <= 64; }
+
+int launch_fit_tc(int m, const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth,
+                  int64_t* sq, int32_t* bad, cudaStream_t st) {
+    switch (m) {
+#define HGA_TC_CASE(M) \
+    case M: return tc::launch_tc_m<M>(pop, n, v, f1, f2, orth, sq, bad, st);
+        HGA_TC_CASE(4) HGA_TC_CASE(8) HGA_TC_CASE(12) HGA_TC_CASE(16) HGA_TC_CASE(20) HGA_TC_CASE(24)
+        HGA_TC_CASE(28) HGA_TC_CASE(32) HGA_TC_CASE(36) HGA_TC_CASE(40) HGA_TC_CASE(44) HGA_TC_CASE(48)
+        HGA_TC_CASE(52) HGA_TC_CASE(56) HGA_TC_CASE(60) HGA_TC_CASE(64)
+#undef HGA_TC_CASE
+        default: return HGA_E_UNSUPPORTED;
+    }
+}
+
+}  // namespace hga

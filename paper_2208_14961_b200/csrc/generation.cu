@@ -618,27 +618,40 @@ static int launch_run_v2(const hga_run_args* a, cudaStream_t st) {
 // Rebuild the select histogram of pop/fit[parity] (state[3]) and reset keys:
 // needed after init and whenever the population was replaced from outside.
 __global__ void k_run2_prepare_zero(RunWs2* ws) {
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < 2 * kR2Bins; b += gridDim.x * blockDim.x)
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < 3 * kR2Bins; b += gridDim.x * blockDim.x)
         (&ws->hist[0][0])[b] = 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ws->bar.count = 0;
         ws->bar.gen = 0;
-        ws->best_key[0] = ws->best_key[1] = ~0ull;
-        ws->par_key[0] = ws->par_key[1] = ~0ull;
         ws->restart_key = ~0ull;
-        ws->kmin[0] = ws->kmin[1] = 0xffffffffu;
-        ws->kmax[0] = ws->kmax[1] = 0u;
+        for (int k = 0; k < 3; ++k) {
+            ws->best_key[k] = ~0ull;
+            ws->par_key[k] = ~0ull;
+            ws->kmin[k] = 0xffffffffu;
+            ws->kmax[k] = 0u;
+        }
     }
 }
 
-__global__ void k_run2_prepare_hist_state(RunWs2* ws, hga_run_args a, int gshift) {
-    const int slot = (int)((a.state[0] + 1) & 1);
-    const int64_t* fit = a.fit[a.state[3]];
+// Histogram (and, for the one-barrier loop, the 16-bit key array padded with
+// 0xFFFF) of pop/fit[state[3]], the population entering generation state[0]+1.
+__global__ void k_run2_prepare_hist_state(RunWs2* ws, hga_run_args a, int gshift, int onebar) {
+    const int64_t gen = a.state[0] + 1;
+    const int slot = onebar ? (int)(gen % 3) : (int)(gen & 1);
+    const int parity = (int)a.state[3];
+    const int64_t* fit = a.fit[parity];
     const int64_t total = 4 * a.n_pairs;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < total; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t kstride = run2_key_stride(a.n_pairs);
+    uint16_t* keys = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(a.ws) + run_ws2_head() + 16 * total);
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < kstride; i0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = i0 + threadIdx.x;
         const bool ok = i < total;
-        hist_add(ws, slot, ok, ok ? (uint32_t)(fit[i] >> gshift) : 0u);
+        const uint32_t key = ok ? (uint32_t)(fit[i] >> gshift) : 0u;
+        if (onebar && i < kstride) {
+            keys[(int64_t)parity * kstride + i] = ok ? (uint16_t)key : (uint16_t)0xFFFF;
+            if (!ok) keys[(int64_t)(parity ^ 1) * kstride + i] = (uint16_t)0xFFFF;
+        }
+        hist_add(ws, slot, ok, key);
     }
 }
 
@@ -646,8 +659,10 @@ static int run2_prepare(const hga_run_args* a, cudaStream_t st) {
     RunWs2* ws = (RunWs2*)a->ws;
     const int64_t total = 4 * a->n_pairs;
     k_run2_prepare_zero<<<64, 256, 0, st>>>(ws);
-    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count_cached() * 8);
-    k_run2_prepare_hist_state<<<std::max(grid, 1), 256, 0, st>>>(ws, *a, run2_granule_shift(a->fit_var));
+    const int64_t kstride = run2_key_stride(a->n_pairs);
+    const int grid = (int)std::min<int64_t>((std::max(total, kstride) + 255) / 256, (int64_t)sm_count_cached() * 8);
+    k_run2_prepare_hist_state<<<std::max(grid, 1), 256, 0, st>>>(ws, *a, run2_granule_shift(a->fit_var),
+                                                                   run2_use_onebar(a) ? 1 : 0);
     return to_rc(cudaGetLastError());
 }
 
@@ -677,7 +692,9 @@ int hga_generation_explicit(uint32_t* pop, int64_t* fit, int64_t n_pairs, int32_
 
 size_t hga_run_ws_bytes(int64_t n_pairs, int32_t m) {
     (void)m;
-    return std::max(run_ws_head() + (size_t)(2 * n_pairs) * 8, run_ws2_head() + (size_t)(8 * n_pairs) * 8);
+    // two-barrier survivor lists (2 x 4N uint64) + one-barrier keys (2 x stride uint16)
+    return std::max(run_ws_head() + (size_t)(2 * n_pairs) * 8,
+                    run_ws2_head() + (size_t)(8 * n_pairs) * 8 + (size_t)run2_key_stride(n_pairs) * 4);
 }
 
 

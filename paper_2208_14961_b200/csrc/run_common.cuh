@@ -84,19 +84,19 @@ __device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) 
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Sense-by-generation grid barrier: bar.sync orders the CTA's writes before
-// thread 0's release-arrive; the last arriver bumps `gen` with a release
-// store, waiters spin with acquire loads (which also drop stale L1 lines).
+// One-atomic grid barrier.  Every CTA adds to one counter: CTA 0 adds
+// 2^31 - (nb - 1), the others 1, so a round adds exactly 2^31 and flips the
+// top bit precisely when the last CTA arrives (the low 31 bits return to 0,
+// so no reset store is needed).  bar.sync orders the CTA's writes before
+// thread 0's acq_rel arrive; waiters poll the top bit with acquire loads.
+// A CTA that races ahead into the next round cannot flip the bit back before
+// every CTA has arrived there too.  `gen` is unused (layout kept).
 __device__ __forceinline__ void grid_sync(Barrier* b) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned int g = ld_acquire_gpu(&b->gen);
-        if (atom_add_acq_rel_gpu(&b->count, 1u) == gridDim.x - 1) {
-            b->count = 0;
-            st_release_gpu(&b->gen, g + 1);
-        } else {
-            while (ld_acquire_gpu(&b->gen) == g) {
-            }
+        const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+        const unsigned int old = atom_add_acq_rel_gpu(&b->count, inc);
+        while (((ld_acquire_gpu(&b->count) ^ old) & 0x80000000u) == 0u) {
         }
     }
     __syncthreads();

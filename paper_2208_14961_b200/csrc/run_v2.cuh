@@ -36,20 +36,29 @@ constexpr int kSelItems = 8;                      // fitness values per thread i
 constexpr int kR2Bins = 32768;
 constexpr int kR2MaxGrid = 2048;
 constexpr int kR2MaxPlan = 128;  // nc + 2 nr <= (m - 1) + m
+constexpr int kRng = 64;          // items per key range (one-barrier select)
+constexpr int kMaxRng = 2048;     // one-barrier select up to 4N = 131,072 matrices
 
+// Per-slot state: the two-barrier loop uses slots gen & 1, the one-barrier
+// loop gen % 3 (see k_run_v3).
 struct RunWs2 {
     Barrier bar;
-    unsigned long long best_key[2];
-    unsigned long long par_key[2];
+    unsigned long long best_key[3];
+    unsigned long long par_key[3];
     unsigned long long restart_key;
-    uint32_t kmin[2];
-    uint32_t kmax[2];
+    uint32_t kmin[3];
+    uint32_t kmax[3];
     uint32_t cnt_lt[kR2MaxGrid];
     uint32_t cnt_eq[kR2MaxGrid];
-    uint32_t hist[2][kR2Bins];
+    uint32_t hist[3][kR2Bins];
     unsigned long long tstamp[64][20];  // HGA_RUN_TIMING: %globaltimer at phase boundaries (CTA 0)
-    // followed by lt_list[4N], eq_list[4N] (uint64 (F << 32) | index): each CTA's survivors, compacted in index order
+    // followed by lt_list[4N], eq_list[4N] (uint64 (F << 32) | index): each CTA's survivors, compacted in index
+    // order (two-barrier loop), then keys[2][run2_key_stride] (uint16 F >> granule per slot, padded with 0xFFFF;
+    // one-barrier loop)
 };
+
+__host__ __device__ inline int64_t run2_key_stride(int64_t n_pairs) { return (4 * n_pairs + kRng - 1) / kRng * kRng; }
+__host__ __device__ inline bool run2_onebar(int64_t n_pairs) { return 4 * n_pairs <= (int64_t)kMaxRng * kRng; }
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -120,28 +129,38 @@ __device__ inline void kth_bin_cg(const uint32_t* h, int bins, uint64_t k, int* 
 }
 
 // One warp: first bin b (in [0, bins)) where the inclusive prefix of h
-// reaches k (1 <= k <= total), and the count strictly below b.
+// reaches k (1 <= k <= total), and the count strictly below b.  Bins are
+// loaded 128 at a time (four independent loads per lane in flight) so a
+// typical key window costs one L2 round trip.
 __device__ inline void kth_bin_warp(const uint32_t* h, int bins, uint64_t k, int* out_bin, uint64_t* out_below) {
     const int lane = threadIdx.x & 31;
     uint64_t run = 0;
-    for (int b0 = 0; b0 < bins; b0 += 32) {
-        const int b = b0 + lane;
-        const uint32_t v = b < bins ? __ldcg(h + b) : 0u;
-        uint64_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+    for (int c0 = 0; c0 < bins; c0 += 128) {
+        uint32_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int b = c0 + 32 * u + lane;
+            v[u] = b < bins ? __ldcg(h + b) : 0u;
         }
-        const bool hit = (run + x >= k) && (run + x - v < k);
-        const unsigned m = __ballot_sync(0xffffffffu, hit);
-        if (m) {
-            if (lane == __ffs(m) - 1) {
-                *out_bin = b;
-                *out_below = run + x - v;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int b = c0 + 32 * u + lane;
+            uint64_t x = v[u];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
             }
-            return;
+            const bool hit = (run + x >= k) && (run + x - v[u] < k);
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (m) {
+                if (lane == __ffs(m) - 1) {
+                    *out_bin = b;
+                    *out_below = run + x - v[u];
+                }
+                return;
+            }
+            run += __shfl_sync(0xffffffffu, x, 31);
         }
-        run += __shfl_sync(0xffffffffu, x, 31);
     }
 }
 
@@ -288,6 +307,7 @@ constexpr int kPlanStride = kR2MaxPlan + 4;  // 33 words: plan rows of 32 childr
 struct TileShared {  // one per 128-thread tile group
     int16_t point[kR2Pairs];
     int32_t pidx[2 * kR2Pairs];  // old-population index of parent row 2q (A) / 2q+1 (B)
+    uint16_t pkey[2 * kR2Pairs]; // its selection key (one-barrier lookup)
     int8_t plan[kTileOff][kPlanStride];
     uint32_t part[kTeam][4][kTileOff];  // child-minor: conflict-free
 };
@@ -297,13 +317,15 @@ struct TileShared {  // one per 128-thread tile group
 // survivors (CTA-major), then the first `quota` eq candidates.  Any fixed
 // bijection works here because the Feistel permutation randomises the slots.
 struct SelView {
-    const uint32_t* lt_pre;  // [nb + 1] exclusive prefix, in shared memory
+    const uint32_t* lt_pre;  // [nb + 1] exclusive prefix, in shared memory (one-barrier: [nrng + 1] over key ranges)
     const uint32_t* eq_pre;
-    int nb;
+    int nb;                  // CTAs (two-barrier) or key ranges (one-barrier)
     int64_t chunk;
     const unsigned long long* lt_list;
     const unsigned long long* eq_list;
     uint32_t total_lt;
+    const uint16_t* keys;    // one-barrier: selection keys of the old population
+    uint32_t tau_key;
 };
 
 __device__ __forceinline__ int upper_bound_u32(const uint32_t* a, int n, uint32_t v) {
@@ -346,10 +368,91 @@ struct TileCtx {
     int nc, nr;
     uint64_t gen;
     int gp, gshift, g;
+    unsigned long long* ts;  // HGA_RUN_TIMING stamps of this generation (CTA 0, group 0), else null
+    uint16_t* keys_new;      // one-barrier: selection keys of the new population, else null
+    int hslot;               // histogram slot of the new population
 };
 
+// 8 uint16 keys: (count < tk) | (count == tk) << 16
+__device__ __forceinline__ uint32_t count8(const uint4& v, uint32_t tk) {
+    const uint32_t t2 = tk | (tk << 16);
+    const uint32_t lt = __popc(__vcmpltu2(v.x, t2)) + __popc(__vcmpltu2(v.y, t2)) + __popc(__vcmpltu2(v.z, t2)) +
+                        __popc(__vcmpltu2(v.w, t2));
+    const uint32_t eq = __popc(__vcmpeq2(v.x, t2)) + __popc(__vcmpeq2(v.y, t2)) + __popc(__vcmpeq2(v.z, t2)) +
+                        __popc(__vcmpeq2(v.w, t2));
+    return (lt >> 4) | ((eq >> 4) << 16);
+}
+
+// One-barrier select, warp 0 of a tile group: the parent of each of the
+// `noff` parent rows is the survivor of rank Feistel^-1(slot).  Lane o finds
+// the key range holding that rank (binary search of the range prefixes in
+// shared memory); then 8-lane teams resolve four lookups per step from the
+// ranges' 64 keys (one 16-byte load per lane, all eight loads in flight).
+__device__ __forceinline__ void select_lookup(const TileCtx& C, TileShared& S, int noff, int64_t slot, bool act) {
+    const SelView& V = *C.V;
+    const int o = threadIdx.x & 31, h = o >> 3, sub = o & 7;
+    int rb = 0;
+    uint32_t rk = 0;
+    bool req = false;
+    if (act) {
+        const uint32_t r = feistel2_inv((uint32_t)slot, *C.fkey);
+        if (r < V.total_lt) {
+            rb = upper_bound_u32(V.lt_pre, V.nb + 1, r) - 1;
+            rk = r - V.lt_pre[rb];
+        } else {
+            const uint32_t e = r - V.total_lt;
+            req = true;
+            rb = upper_bound_u32(V.eq_pre, V.nb + 1, e) - 1;
+            rk = e - V.eq_pre[rb];
+        }
+    }
+    uint4 kv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int j = 4 * i + h;
+        const int bj = __shfl_sync(0xffffffffu, rb, j);
+        kv[i] = j < noff ? __ldcg(reinterpret_cast<const uint4*>(V.keys + (int64_t)bj * kRng) + sub)
+                         : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    }
+    const uint32_t t2 = V.tau_key | (V.tau_key << 16);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int j = 4 * i + h;
+        const uint32_t kj = __shfl_sync(0xffffffffu, rk, j);
+        const bool eqj = __shfl_sync(0xffffffffu, req, j);
+        const int bj = __shfl_sync(0xffffffffu, rb, j);
+        const uint32_t w[4] = {kv[i].x, kv[i].y, kv[i].z, kv[i].w};
+        uint32_t mask = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t c = eqj ? __vcmpeq2(w[u], t2) : __vcmpltu2(w[u], t2);
+            mask |= ((c & 1u) << (2 * u)) | (((c >> 16) & 1u) << (2 * u + 1));
+        }
+        const uint32_t cnt = __popc(mask);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 8; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d, 8);
+            if (sub >= d) incl += y;
+        }
+        const uint32_t excl = incl - cnt;
+        if (j < noff && kj >= excl && kj < incl) {
+            uint32_t mm = mask;
+            for (uint32_t z = kj - excl; z > 0; --z) mm &= mm - 1u;
+            const int u = __ffs(mm) - 1;
+            S.pidx[j] = bj * kRng + 8 * sub + u;
+            S.pkey[j] = (uint16_t)(w[u >> 1] >> (16 * (u & 1)));
+        }
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void tile_stamp(const TileCtx& C, int slot) {
+    if (C.ts != nullptr && (threadIdx.x & (kR2Threads - 1)) == 0) C.ts[slot] = gtimer();
+}
+
 // Step a: parents by rank (warp 0), crossover points (warp 3), mutation plans (warps 1-3).
-template <int M>
+template <int M, bool ONE>
 __device__ __forceinline__ void tile_prepare(const TileCtx& C, TileShared& S, int64_t p0, int cnt, LocalAcc& L) {
     const int t = threadIdx.x & (kR2Threads - 1), k = t >> 5, o = t & 31;
     const int noff = 2 * cnt;
@@ -358,19 +461,27 @@ __device__ __forceinline__ void tile_prepare(const TileCtx& C, TileShared& S, in
     const int64_t N = C.N;
     if (k == 0) {
         const bool act = o < noff;
+        const int64_t slot = (int64_t)(o & 1) * N + p0 + (o >> 1);
         int64_t f = 0;
-        if (act) {
-            const int q = o >> 1, b = o & 1;
-            const int64_t slot = (int64_t)b * N + p0 + q;
+        if constexpr (ONE) {
+            select_lookup(C, S, noff, slot, act);
+            if (act) {
+                const uint16_t pk = S.pkey[o];
+                f = (int64_t)pk << C.gshift;
+                C.keys_new[slot] = pk;
+            }
+        } else if (act) {
             const unsigned long long kv = survivor_by_rank(*C.V, feistel2_inv((uint32_t)slot, *C.fkey));
             S.pidx[o] = (int32_t)(kv & 0xffffffffu);
             f = (int64_t)(kv >> 32);
+        }
+        if (act) {
             C.f_new[slot] = f;
             const unsigned long long key = ((unsigned long long)f << 32) | (unsigned long long)slot;
             L.best = min(L.best, key);
             L.pbest = min(L.pbest, key);
         }
-        local_hist_add(L, C.ws, C.gp ^ 1, act, (uint32_t)(f >> C.gshift));
+        local_hist_add(L, C.ws, C.hslot, act, (uint32_t)(f >> C.gshift));
     } else {
         if (k == kTeam - 1 && o < cnt) {
             const int64_t p = p0 + o;
@@ -425,6 +536,7 @@ __device__ __forceinline__ void tile_compute(const TileCtx& C, TileShared& S, ui
         reinterpret_cast<uint4*>(C.pop_new + ((int64_t)b * N + p0 + q) * G::MW)[u] = rows[(2 * q + b) * G::STU + u];
     }
     group_sync(g);
+    tile_stamp(C, 14);
     // c. column-block crossover in place
     for (int x = t; x < cnt * M; x += kR2Threads) {
         const int q = x / M, j = x - q * M;
@@ -440,6 +552,7 @@ __device__ __forceinline__ void tile_compute(const TileCtx& C, TileShared& S, ui
         }
     }
     group_sync(g);
+    tile_stamp(C, 15);
     // d. mutation: thread (k, o) handles plan entries jc = k, k + 4, ...; an
     //    entry whose column already appeared earlier is skipped, and the first
     //    occurrence applies the column's row-pair sequence once per occurrence
@@ -470,6 +583,7 @@ __device__ __forceinline__ void tile_compute(const TileCtx& C, TileShared& S, ui
         }
     }
     group_sync(g);
+    tile_stamp(C, 16);
     // e. pair chain, a quarter per warp
     if (o < noff) {
         uint32_t c[G::MW];
@@ -494,6 +608,7 @@ __device__ __forceinline__ void tile_compute(const TileCtx& C, TileShared& S, ui
         S.part[k][3][o] = s.spp;
     }
     group_sync(g);
+    tile_stamp(C, 17);
     // f. warp 0: children's fitness, best key, next histogram
     if (k == 0) {
         const bool active = o < noff;
@@ -510,10 +625,12 @@ __device__ __forceinline__ void tile_compute(const TileCtx& C, TileShared& S, ui
             value = variant_value<M, VM>(s, G::NP);
             const int64_t slot = 2 * N + (int64_t)(o & 1) * N + p0 + (o >> 1);
             C.f_new[slot] = value;
+            if (C.keys_new != nullptr) C.keys_new[slot] = (uint16_t)(value >> C.gshift);
             L.best = min(L.best, ((unsigned long long)value << 32) | (unsigned long long)slot);
         }
-        local_hist_add(L, C.ws, C.gp ^ 1, active, (uint32_t)(value >> C.gshift));
+        local_hist_add(L, C.ws, C.hslot, active, (uint32_t)(value >> C.gshift));
     }
+    tile_stamp(C, 18);
     // g. coalesced store of the children (O1 block, then O2 block)
     for (int x = t; x < noff * G::U; x += kR2Threads) {
         const int b = x / (cnt * G::U);
@@ -522,9 +639,10 @@ __device__ __forceinline__ void tile_compute(const TileCtx& C, TileShared& S, ui
         reinterpret_cast<uint4*>(C.pop_new + (2 * N + (int64_t)b * N + p0 + q) * G::MW)[u] = rows[(2 * q + b) * G::STU + u];
     }
     group_sync(g);
+    tile_stamp(C, 19);
 }
 
-template <int M, int VM>
+template <int M, int VM, bool ONE>
 __device__ __forceinline__ void group_tiles(const TileCtx& C, int64_t first, int64_t stride, int64_t ntiles,
                                             uint4* rows0, uint4* rows1, TileShared* S0, TileShared* S1,
                                             LocalAcc& L) {
@@ -533,20 +651,24 @@ __device__ __forceinline__ void group_tiles(const TileCtx& C, int64_t first, int
     uint4* rows[2] = {rows0, rows1};
     TileShared* S[2] = {S0, S1};
     auto cnt_of = [&](int64_t tile) { return (int)min((int64_t)kR2Pairs, N - tile * kR2Pairs); };
-    tile_prepare<M>(C, *S[0], first * kR2Pairs, cnt_of(first), L);
+    tile_prepare<M, ONE>(C, *S[0], first * kR2Pairs, cnt_of(first), L);
     group_sync(C.g);
+    tile_stamp(C, 12);
     tile_gather<M>(C, *S[0], rows[0], cnt_of(first));
     cp_async_commit();
     int cur = 0;
+    TileCtx Cs = C;
     for (int64_t tile = first; tile < ntiles; tile += stride) {
         const int64_t nxt = tile + stride;
-        if (nxt < ntiles) tile_prepare<M>(C, *S[cur ^ 1], nxt * kR2Pairs, cnt_of(nxt), L);
+        if (nxt < ntiles) tile_prepare<M, ONE>(C, *S[cur ^ 1], nxt * kR2Pairs, cnt_of(nxt), L);
         group_sync(C.g);
         if (nxt < ntiles) tile_gather<M>(C, *S[cur ^ 1], rows[cur ^ 1], cnt_of(nxt));
         cp_async_commit();
         cp_async_wait<1>();
         group_sync(C.g);
-        tile_compute<M, VM>(C, *S[cur], rows[cur], tile * kR2Pairs, cnt_of(tile), L);
+        if (tile == first) tile_stamp(C, 13);
+        tile_compute<M, VM>(Cs, *S[cur], rows[cur], tile * kR2Pairs, cnt_of(tile), L);
+        Cs.ts = nullptr;  // stamps for the first tile only
         cur ^= 1;
     }
     cp_async_wait<0>();
@@ -554,7 +676,54 @@ __device__ __forceinline__ void group_tiles(const TileCtx& C, int64_t first, int
 
 constexpr int kMaxNb = 512;  // prefix scan: one pass of <= 16 warps
 
-template <int M, int VM, int GROUPS>
+// Block-wide exclusive prefix of packed per-range counts (lt | eq << 16) into
+// lt_pre / eq_pre[0..n]; entry n holds the totals.  Ends without a barrier.
+__device__ inline void scan_ranges(const uint32_t* cnt, int n, uint32_t* lt_pre, uint32_t* eq_pre, uint64_t* sscr) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+    const int per = (n + nt - 1) / nt;
+    const int r0 = min(n, tid * per), r1 = min(n, r0 + per);
+    uint64_t mine = 0;
+    for (int r = r0; r < r1; ++r) {
+        const uint32_t c = cnt[r];
+        mine += ((uint64_t)(c & 0xffffu) << 32) | (c >> 16);
+    }
+    uint64_t x = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sscr[wid] = x;
+    __syncthreads();
+    uint64_t run = x - mine, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+        const uint64_t t = sscr[w];
+        if (w < wid) run += t;
+        tot += t;
+    }
+    for (int r = r0; r < r1; ++r) {
+        lt_pre[r] = (uint32_t)(run >> 32);
+        eq_pre[r] = (uint32_t)run;
+        const uint32_t c = cnt[r];
+        run += ((uint64_t)(c & 0xffffu) << 32) | (c >> 16);
+    }
+    if (tid == 0) {
+        lt_pre[n] = (uint32_t)(tot >> 32);
+        eq_pre[n] = (uint32_t)tot;
+    }
+}
+
+// ONE = one grid barrier per generation (HGA_RUN_ONE_BARRIER, 4N <= kMaxRng * kRng): the tiles
+// also store each new matrix's 16-bit selection key; after the barrier every
+// CTA reads ALL keys (2 bytes per matrix, L2 resident), so every CTA knows
+// the per-range survivor counts of the whole population and the survivor
+// lists never need to be materialised (and no second barrier is needed to
+// publish them).  Per-generation slots rotate mod 3 so that the histogram /
+// key range / best keys being read, being accumulated and being retired are
+// always different slots.  Both variants select the same survivors with the
+// same ranks, so they produce identical runs.  Measured: ONE is slower at
+// order 20 (22.8 vs 17.2 us/generation: reading all keys and the 8-lane
+// lookups cost more than the second barrier saves), so it is opt-in.
+template <int M, int VM, int GROUPS, bool ONE>
 __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t sscr[32];
@@ -563,7 +732,8 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     __shared__ uint32_t s_hist[kWin];
     __shared__ uint32_t s_kmin, s_kmax;
     __shared__ unsigned long long s_best, s_pbest;
-    __shared__ uint32_t s_ltpre[kMaxNb + 1], s_eqpre[kMaxNb + 1];
+    __shared__ uint32_t s_ltpre[kMaxRng + 1], s_eqpre[kMaxRng + 1];
+    __shared__ uint32_t s_cnt[ONE ? kMaxRng : 1];
 
     using G = RunGeom<M>;
     const hga_run_args& A = P.a;
@@ -571,6 +741,9 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     unsigned long long* lt_list = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(A.ws) + run_ws2_head());
     const int64_t N = A.n_pairs, half = 2 * N, total = 4 * N;
     unsigned long long* eq_list = lt_list + total;
+    uint16_t* keys_base = reinterpret_cast<uint16_t*>(eq_list + total);
+    const int64_t kstride = run2_key_stride(N);
+    const int nrng = (int)(kstride / kRng);
     const int nb = gridDim.x, bid = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
     const int g = tid / kR2Threads;
     const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
@@ -598,12 +771,18 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     const bool force = (A.flags & HGA_RUN_FORCE) != 0;
     bool stop = !force && A.state[5] != 0;
     const bool timing = (A.flags & HGA_RUN_TIMING) != 0 && bid == 0 && tid == 0;
+    const bool timing_blk = (A.flags & HGA_RUN_TIMING) != 0 && bid == 0;
     uint32_t next_kmin = 0, next_kmax = 0;
     bool have_krange = false;
 
     for (int64_t gi = 0; gi < A.gens_this_call && !stop; ++gi) {
         const int64_t gen = iter + 1;
         const int gp = (int)(gen & 1);  // histogram / key slot of the population entering `gen`
+        const int s0 = (int)(gen % 3), s1 = (int)((gen + 1) % 3), s2 = (int)((gen + 2) % 3);
+        const int rslot = ONE ? s0 : gp;        // select histogram of the population entering gen
+        const int hslot = ONE ? s1 : (gp ^ 1);  // histogram / key range of the new population
+        const int bslot = ONE ? s1 : gp;        // best / parent-best keys of the new population
+        const uint16_t* kold = keys_base + (int64_t)parity * kstride;
         const uint32_t* pop_old = A.pop[parity];
         uint32_t* pop_new = A.pop[parity ^ 1];
         const int64_t* f_old = A.fit[parity];
@@ -613,113 +792,175 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
             ws->tstamp[gi][10] = clock64();
         }
 
-        // ---- B: threshold, tie quota, local survivor lists
-        // first batch of fitness values: independent of tau, so load it under the histogram scan
-        int64_t fpre[kSelItems];
-        if (wid < pw_sel) load_items(f_old, lo + (int64_t)tid * kSelItems, hi, fpre);
-        if (!have_krange) {  // otherwise read with the bookkeeping loads of the previous generation
-            next_kmin = __ldcg(&ws->kmin[gp]);
-            next_kmax = __ldcg(&ws->kmax[gp]);
-        }
-        const uint32_t kmin = next_kmin, kmax = next_kmax;
-        if (wid == 0) kth_bin_warp(&ws->hist[gp][kmin], (int)(kmax - kmin + 1), (uint64_t)half, &s_bin, &s_below);
-        __syncthreads();
-        const int64_t tau = (int64_t)(kmin + (uint32_t)s_bin) << gshift;
-        const uint32_t quota = (uint32_t)((uint64_t)half - s_below);
-        {
-            uint32_t lt_run = 0, eq_run = 0;
-            const int64_t span = (int64_t)pw_sel * 32 * kSelItems;
-            for (int64_t b0 = lo; b0 < hi; b0 += span) {
-                const int64_t i0 = b0 + (int64_t)tid * kSelItems;
-                int64_t f[kSelItems];
-                uint32_t v = 0, x = 0;
-                if (wid < pw_sel) {
-                    if (b0 == lo) {
+        uint32_t kmin = 0, kmax = 0, tau_key = 0;
+        if constexpr (ONE) {
+            // ---- one-barrier select: threshold, per-range counts of the whole population
+            const int team = wid * 4 + (lane >> 3), sub = lane & 7, nteam = nw * 4;
+            uint4 kb[8];
 #pragma unroll
-                        for (int u = 0; u < kSelItems; ++u) f[u] = fpre[u];
-                    } else {
-                        load_items(f_old, i0, hi, f);
-                    }
+            for (int i = 0; i < 8; ++i) {
+                const int r = team + nteam * i;
+                kb[i] = r < nrng ? __ldcg(reinterpret_cast<const uint4*>(kold + (int64_t)r * kRng) + sub)
+                                 : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+            }
+            if (!have_krange) {
+                next_kmin = __ldcg(&ws->kmin[rslot]);
+                next_kmax = __ldcg(&ws->kmax[rslot]);
+            }
+            kmin = next_kmin;
+            kmax = next_kmax;
+            uint32_t zmin = 1u, zmax = 0u;  // CTA 0 retires slot s2 (last read before the previous barrier)
+            if (bid == 0) {
+                zmin = __ldcg(&ws->kmin[s2]);
+                zmax = __ldcg(&ws->kmax[s2]);
+            }
+            if (wid == 0) kth_bin_warp(&ws->hist[rslot][kmin], (int)(kmax - kmin + 1), (uint64_t)half, &s_bin, &s_below);
+            __syncthreads();
+            if (timing && gi < 64) ws->tstamp[gi][3] = gtimer();
+            tau_key = kmin + (uint32_t)s_bin;
+            if (bid == 0 && zmin <= zmax)
+                for (uint32_t b = zmin + tid; b <= zmax; b += nt) ws->hist[s2][b] = 0;
+            for (int r0 = 0; r0 < nrng; r0 += nteam * 8) {
+                if (r0 > 0) {
 #pragma unroll
-                    for (int u = 0; u < kSelItems; ++u) {
-                        const bool in = i0 + u < hi;
-                        v += (in && f[u] < tau) ? 0x10000u : 0u;
-                        v += (in && f[u] == tau) ? 1u : 0u;
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = r0 + team + nteam * i;
+                        kb[i] = r < nrng ? __ldcg(reinterpret_cast<const uint4*>(kold + (int64_t)r * kRng) + sub)
+                                         : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
                     }
-                    x = v;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint32_t c = count8(kb[i], tau_key);
+                    c += __shfl_xor_sync(0xffffffffu, c, 4);
+                    c += __shfl_xor_sync(0xffffffffu, c, 2);
+                    c += __shfl_xor_sync(0xffffffffu, c, 1);
+                    const int r = r0 + team + nteam * i;
+                    if (sub == 0 && r < nrng) s_cnt[r] = c;
+                }
+            }
+            __syncthreads();
+            scan_ranges(s_cnt, nrng, s_ltpre, s_eqpre, sscr);
+            __syncthreads();
+            if (bid == 0 && tid == 0) {
+                ws->kmin[s2] = 0xffffffffu;
+                ws->kmax[s2] = 0u;
+                ws->best_key[s2] = ~0ull;
+                ws->par_key[s2] = ~0ull;
+            }
+            if (timing && gi < 64) ws->tstamp[gi][2] = ws->tstamp[gi][1] = gtimer();
+        } else {
+            // ---- B: threshold, tie quota, local survivor lists
+            // first batch of fitness values: independent of tau, so load it under the histogram scan
+            int64_t fpre[kSelItems];
+            if (wid < pw_sel) load_items(f_old, lo + (int64_t)tid * kSelItems, hi, fpre);
+            if (!have_krange) {  // otherwise read with the bookkeeping loads of the previous generation
+                next_kmin = __ldcg(&ws->kmin[rslot]);
+                next_kmax = __ldcg(&ws->kmax[rslot]);
+            }
+            kmin = next_kmin;
+            kmax = next_kmax;
+            if (wid == 0) kth_bin_warp(&ws->hist[rslot][kmin], (int)(kmax - kmin + 1), (uint64_t)half, &s_bin, &s_below);
+            __syncthreads();
+            if (timing && gi < 64) ws->tstamp[gi][3] = gtimer();
+            const int64_t tau = (int64_t)(kmin + (uint32_t)s_bin) << gshift;
+            const uint32_t quota = (uint32_t)((uint64_t)half - s_below);
+            {
+                uint32_t lt_run = 0, eq_run = 0;
+                const int64_t span = (int64_t)pw_sel * 32 * kSelItems;
+                for (int64_t b0 = lo; b0 < hi; b0 += span) {
+                    const int64_t i0 = b0 + (int64_t)tid * kSelItems;
+                    int64_t f[kSelItems];
+                    uint32_t v = 0, x = 0;
+                    if (wid < pw_sel) {
+                        if (b0 == lo) {
+    #pragma unroll
+                            for (int u = 0; u < kSelItems; ++u) f[u] = fpre[u];
+                        } else {
+                            load_items(f_old, i0, hi, f);
+                        }
+    #pragma unroll
+                        for (int u = 0; u < kSelItems; ++u) {
+                            const bool in = i0 + u < hi;
+                            v += (in && f[u] < tau) ? 0x10000u : 0u;
+                            v += (in && f[u] == tau) ? 1u : 0u;
+                        }
+                        x = v;
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                            if (lane >= o) x += y;
+                        }
+                        if (lane == 31) sscr[wid] = x;
+                    }
+                    __syncthreads();
+                    uint32_t wbase = 0, tot = 0;
+                    for (int w = 0; w < pw_sel; ++w) {
+                        const uint32_t tw = (uint32_t)sscr[w];
+                        if (w < wid) wbase += tw;
+                        tot += tw;
+                    }
+                    if (wid < pw_sel) {
+                        uint32_t excl = wbase + x - v;
+    #pragma unroll
+                        for (int u = 0; u < kSelItems; ++u) {
+                            const bool in = i0 + u < hi;
+                            const unsigned long long kv = ((unsigned long long)f[u] << 32) | (unsigned long long)(i0 + u);
+                            if (in && f[u] < tau) lt_list[lo + lt_run + (excl >> 16)] = kv;
+                            if (in && f[u] == tau) eq_list[lo + eq_run + (excl & 0xffffu)] = kv;
+                            excl += ((in && f[u] < tau) ? 0x10000u : 0u) + ((in && f[u] == tau) ? 1u : 0u);
+                        }
+                    }
+                    lt_run += tot >> 16;
+                    eq_run += tot & 0xffffu;
+                    __syncthreads();
+                }
+                if (tid == 0) {
+                    ws->cnt_lt[bid] = lt_run;
+                    ws->cnt_eq[bid] = eq_run;
+                }
+            }
+            if (timing && gi < 64) ws->tstamp[gi][1] = gtimer();
+            grid_sync(&ws->bar);
+            if (timing && gi < 64) ws->tstamp[gi][2] = gtimer();
+
+            // ---- E: prefix of the survivor counts, then the offspring tiles
+            if (bid == 0) {
+                for (uint32_t b = kmin + tid; b <= kmax; b += nt) ws->hist[rslot][b] = 0;
+            }
+            {
+                // exclusive prefix of cnt_lt / cnt_eq over the nb CTAs (nb <= kMaxNb), pw_pre warps
+                uint64_t x = 0, v = 0;
+                const int b = tid;
+                if (wid < pw_pre) {
+                    const uint32_t a = b < nb ? __ldcg(&ws->cnt_lt[b]) : 0u;
+                    const uint32_t e = b < nb ? __ldcg(&ws->cnt_eq[b]) : 0u;
+                    x = v = ((uint64_t)a << 32) | e;
                     for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
                         if (lane >= o) x += y;
                     }
                     if (lane == 31) sscr[wid] = x;
                 }
                 __syncthreads();
-                uint32_t wbase = 0, tot = 0;
-                for (int w = 0; w < pw_sel; ++w) {
-                    const uint32_t tw = (uint32_t)sscr[w];
-                    if (w < wid) wbase += tw;
-                    tot += tw;
-                }
-                if (wid < pw_sel) {
-                    uint32_t excl = wbase + x - v;
-#pragma unroll
-                    for (int u = 0; u < kSelItems; ++u) {
-                        const bool in = i0 + u < hi;
-                        const unsigned long long kv = ((unsigned long long)f[u] << 32) | (unsigned long long)(i0 + u);
-                        if (in && f[u] < tau) lt_list[lo + lt_run + (excl >> 16)] = kv;
-                        if (in && f[u] == tau) eq_list[lo + eq_run + (excl & 0xffffu)] = kv;
-                        excl += ((in && f[u] < tau) ? 0x10000u : 0u) + ((in && f[u] == tau) ? 1u : 0u);
+                if (wid < pw_pre) {
+                    uint64_t wbase = 0, tot = 0;
+                    for (int w = 0; w < pw_pre; ++w) {
+                        if (w < wid) wbase += sscr[w];
+                        tot += sscr[w];
+                    }
+                    const uint64_t excl = wbase + x - v;
+                    if (b < nb) {
+                        s_ltpre[b] = (uint32_t)(excl >> 32);
+                        s_eqpre[b] = (uint32_t)(excl & 0xffffffffu);
+                    }
+                    if (tid == 0) {
+                        s_ltpre[nb] = (uint32_t)(tot >> 32);
+                        s_eqpre[nb] = (uint32_t)(tot & 0xffffffffu);
                     }
                 }
-                lt_run += tot >> 16;
-                eq_run += tot & 0xffffu;
-                __syncthreads();
-            }
-            if (tid == 0) {
-                ws->cnt_lt[bid] = lt_run;
-                ws->cnt_eq[bid] = eq_run;
             }
         }
-        if (timing && gi < 64) ws->tstamp[gi][1] = gtimer();
-        grid_sync(&ws->bar);
-        if (timing && gi < 64) ws->tstamp[gi][2] = gtimer();
-
-        // ---- E: prefix of the survivor counts, then the offspring tiles
-        if (bid == 0) {
-            for (uint32_t b = kmin + tid; b <= kmax; b += nt) ws->hist[gp][b] = 0;
-        }
-        {
-            // exclusive prefix of cnt_lt / cnt_eq over the nb CTAs (nb <= kMaxNb), pw_pre warps
-            uint64_t x = 0, v = 0;
-            const int b = tid;
-            if (wid < pw_pre) {
-                const uint32_t a = b < nb ? __ldcg(&ws->cnt_lt[b]) : 0u;
-                const uint32_t e = b < nb ? __ldcg(&ws->cnt_eq[b]) : 0u;
-                x = v = ((uint64_t)a << 32) | e;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                if (lane == 31) sscr[wid] = x;
-            }
-            __syncthreads();
-            if (wid < pw_pre) {
-                uint64_t wbase = 0, tot = 0;
-                for (int w = 0; w < pw_pre; ++w) {
-                    if (w < wid) wbase += sscr[w];
-                    tot += sscr[w];
-                }
-                const uint64_t excl = wbase + x - v;
-                if (b < nb) {
-                    s_ltpre[b] = (uint32_t)(excl >> 32);
-                    s_eqpre[b] = (uint32_t)(excl & 0xffffffffu);
-                }
-                if (tid == 0) {
-                    s_ltpre[nb] = (uint32_t)(tot >> 32);
-                    s_eqpre[nb] = (uint32_t)(tot & 0xffffffffu);
-                }
-            }
-        }
+        if (timing && gi < 64) ws->tstamp[gi][5] = gtimer();
         LocalAcc L;
         L.s_hist = s_hist;
         L.wbase = kmin > 256u ? kmin - 256u : 0u;
@@ -735,12 +976,15 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
             s_pbest = ~0ull;
         }
         __syncthreads();
-        SelView V{s_ltpre, s_eqpre, nb, chunk, lt_list, eq_list, s_ltpre[nb]};
+        SelView V = ONE ? SelView{s_ltpre, s_eqpre, nrng, 0, nullptr, nullptr, s_ltpre[nrng], kold, tau_key}
+                        : SelView{s_ltpre, s_eqpre, nb, chunk, lt_list, eq_list, s_ltpre[nb], nullptr, 0u};
         const FeistelKey fkey = make_feistel_key(draw4(A.seed, 0, 0, (uint64_t)gen, (uint32_t)kPSelect), (uint32_t)half);
         if (timing && gi < 64) ws->tstamp[gi][7] = gtimer();
         {
-            TileCtx C{&A, ws, &V, &fkey, pop_old, pop_new, f_new, N, nc, nr, (uint64_t)gen, gp, gshift, g};
-            group_tiles<M, VM>(C, (int64_t)bid * GROUPS + g, (int64_t)nb * GROUPS, ntiles, rows0, rows1, S0, S1, L);
+            TileCtx C{&A, ws, &V, &fkey, pop_old, pop_new, f_new, N, nc, nr, (uint64_t)gen, gp, gshift, g,
+                      (timing_blk && g == 0 && gi < 64) ? ws->tstamp[gi] : nullptr,
+                      ONE ? keys_base + (int64_t)(parity ^ 1) * kstride : nullptr, hslot};
+            group_tiles<M, VM, ONE>(C, (int64_t)bid * GROUPS + g, (int64_t)nb * GROUPS, ntiles, rows0, rows1, S0, S1, L);
         }
         if (timing && gi < 64) ws->tstamp[gi][8] = gtimer();
         // flush the CTA's histogram window, key range and best keys
@@ -760,12 +1004,12 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
             }
             __syncthreads();
             for (int b = tid; b < kWin; b += nt)
-                if (s_hist[b]) atomicAdd(&ws->hist[gp ^ 1][L.wbase + b], s_hist[b]);
+                if (s_hist[b]) atomicAdd(&ws->hist[hslot][L.wbase + b], s_hist[b]);
             if (tid == 0) {
-                if (s_best != ~0ull) atomicMin(&ws->best_key[gp], s_best);
-                if (s_pbest != ~0ull) atomicMin(&ws->par_key[gp], s_pbest);
-                if (s_kmin != 0xffffffffu) atomicMin(&ws->kmin[gp ^ 1], s_kmin);
-                atomicMax(&ws->kmax[gp ^ 1], s_kmax);
+                if (s_best != ~0ull) atomicMin(&ws->best_key[bslot], s_best);
+                if (s_pbest != ~0ull) atomicMin(&ws->par_key[bslot], s_pbest);
+                if (s_kmin != 0xffffffffu) atomicMin(&ws->kmin[hslot], s_kmin);
+                atomicMax(&ws->kmax[hslot], s_kmax);
             }
         }
         if (timing && gi < 64) ws->tstamp[gi][9] = gtimer();
@@ -777,9 +1021,9 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
 
         // ---- F: bookkeeping (identical in every CTA)
         {
-            const unsigned long long key = __ldcg(&ws->best_key[gp]);
-            next_kmin = __ldcg(&ws->kmin[gp ^ 1]);  // key range of the next generation's histogram
-            next_kmax = __ldcg(&ws->kmax[gp ^ 1]);
+            const unsigned long long key = __ldcg(&ws->best_key[bslot]);
+            next_kmin = __ldcg(&ws->kmin[hslot]);  // key range of the next generation's histogram
+            next_kmax = __ldcg(&ws->kmax[hslot]);
             have_krange = true;
             const int64_t v = (int64_t)(key >> 32);
             const int64_t idx = (int64_t)(key & 0xffffffffu);
@@ -795,7 +1039,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
                     for (int64_t t2 = tid; t2 < G::MW; t2 += nt) A.best_matrix[t2] = __ldcg(pop_new + idx * G::MW + t2);
                     if (tid == 0) A.state[4] = idx;
                 }
-                if (tid == 0) {
+                if (!ONE && tid == 0) {
                     ws->best_key[gp ^ 1] = ~0ull;
                     ws->par_key[gp ^ 1] = ~0ull;
                     ws->kmin[gp] = 0xffffffffu;
@@ -807,7 +1051,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
                 run >= A.stall_window && last_val > 0) {
                 // stall restart (engine.py:482-494): fresh offspring, parents kept,
                 // next-generation histogram rebuilt from scratch
-                const int ngp = gp ^ 1;
+                const int ngp = hslot;
                 const uint32_t omin = __ldcg(&ws->kmin[ngp]), omax = __ldcg(&ws->kmax[ngp]);
                 grid_sync(&ws->bar);
                 if (bid == 0) {
@@ -850,6 +1094,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
                             pair_sums<M, VM, 1>(c, s);
                             fv = variant_value<M, VM>(s, G::NP);
                             f_new[k] = fv;
+                            if constexpr (ONE) keys_base[(int64_t)parity * kstride + k] = (uint16_t)(fv >> gshift);
                         } else {
                             fv = __ldcg(f_new + k);
                         }
@@ -860,7 +1105,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
                 }
                 grid_sync(&ws->bar);
                 const unsigned long long rk = __ldcg(&ws->restart_key);
-                const unsigned long long pk = __ldcg(&ws->par_key[gp]);
+                const unsigned long long pk = __ldcg(&ws->par_key[bslot]);
                 const unsigned long long k2 = min(rk, pk);
                 const int64_t v2 = (int64_t)(k2 >> 32);
                 if (v2 < best) {
@@ -892,6 +1137,9 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
 
 int run2_granule_shift(uint32_t fit_var);
 bool run2_supported(const hga_run_args* a);
+inline bool run2_use_onebar(const hga_run_args* a) {
+    return run2_onebar(a->n_pairs) && (a->flags & HGA_RUN_ONE_BARRIER) != 0;
+}
 
 template <int M>
 int launch_run_v2_m(const hga_run_args* a, cudaStream_t st);
@@ -906,15 +1154,14 @@ constexpr int run_groups() {
     return M <= 24 ? 5 : (M <= 36 ? 4 : 2);
 }
 
-// Definition used by the per-order instantiation files run_m<M>.cu.
-template <int M, int VM>
-int launch_run_v2_mv(const hga_run_args* a, cudaStream_t st) {
+template <int M, int VM, bool ONE>
+int launch_run_v2_k(const hga_run_args* a, cudaStream_t st) {
     constexpr int GROUPS = run_groups<M>();
     Run2Params P;
     P.a = *a;
     P.gshift = run2_granule_shift(a->fit_var);
     const int smem = GROUPS * (2 * kTileOff * RunGeom<M>::STU * 16 + 2 * (int)((sizeof(TileShared) + 15) & ~(size_t)15));
-    auto kern = k_run_v3<M, VM, GROUPS>;
+    auto kern = k_run_v3<M, VM, GROUPS, ONE>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -930,6 +1177,13 @@ int launch_run_v2_mv(const hga_run_args* a, cudaStream_t st) {
     const int grid = std::min(std::min(sm_count_cached() * std::min(per_sm, 2), kMaxNb), GROUPS * kR2Threads);
     void* params[] = {&P};
     return to_rc(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kR2Threads * GROUPS), params, smem, st));
+}
+
+// Definition used by the per-order instantiation files run_m<M>.cu.
+template <int M, int VM>
+int launch_run_v2_mv(const hga_run_args* a, cudaStream_t st) {
+    if (run2_use_onebar(a)) return launch_run_v2_k<M, VM, true>(a, st);
+    return launch_run_v2_k<M, VM, false>(a, st);
 }
 
 template <int M>

@@ -81,6 +81,7 @@ MAX_RESIDENT_ORDER = 128                         # register-resident column word
 _P_INIT, _P_SELECT, _P_CROSSOVER, _P_MUT_COL, _P_MUT_ROW_A, _P_MUT_ROW_B, _P_RESTART = 1, 2, 3, 4, 5, 6, 7
 
 DEBUG_CHECKS = False
+_RUN_FLAGS = 0  # extra hga_run_args.flags for every persistent-loop call (tests: RUN_TWO_BARRIER)
 
 
 def _sid(purpose: int, generation: int = 0, matrix: int = 0, column: int = 0) -> int:
@@ -498,6 +499,7 @@ class _Resident:
         a.best_matrix = self.best_packed.data_ptr()
         a.ws = self.run_ws.data_ptr()
         a.ws_bytes = self.run_ws.shape[0]
+        a.flags = _RUN_FLAGS
         return a
 
     def ensure_trace(self, upto: int) -> None:
@@ -659,7 +661,7 @@ def _run_device(state: SearchState, gens: int, force: bool = False) -> None:
     a = res.run_args()
     a.gens_this_call = gens
     if force:
-        a.flags = RUN_FORCE
+        a.flags |= RUN_FORCE
     check(lib.hga_run(a, stream_ptr()), "hga_run")
     _sync_from_device(state)
 
@@ -681,7 +683,7 @@ def step(state, workers: int = 1):
         res.ensure_trace(state.iteration + 1)
         a = res.run_args()
         a.gens_this_call = 1
-        a.flags = RUN_FORCE
+        a.flags |= RUN_FORCE
         check(lib.hga_run(a, stream_ptr()), "hga_run")
         _sync_from_device(state)
     if DEBUG_CHECKS:

@@ -8,7 +8,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2208_14961_b200 import engine  # noqa: E402
-from paper_2208_14961_b200._lib import RUN_FORCE, RUN_TIMING, check, lib  # noqa: E402
+from paper_2208_14961_b200._lib import RUN_FORCE, RUN_TIMING, RUN_ONE_BARRIER, check, lib  # noqa: E402
 
 # ramp the SM clock first (~0.5 s of integer work; a bf16 GEMM burn drives the
 # part into its power cap and leaves the clocks low for the measurement)
@@ -19,14 +19,17 @@ while __import__("time").time() - _t0 < 0.5:
 torch.cuda.synchronize()
 del _pop
 
-for m, N in ((12, 1000), (20, 10_000), (28, 31_250), (36, 312_500)):
+CASES = [(12, 1000, 0), (20, 10_000, 0), (20, 10_000, RUN_ONE_BARRIER), (28, 31_250, 0),
+         (28, 31_250, RUN_ONE_BARRIER), (36, 312_500, 0)]
+for m, N, xflags in CASES:
+    engine._RUN_FLAGS = xflags
     cfg = engine.GAConfig(order=m, population=N, seed=1, fitness="f2", mutation_cols=4, mutation_row_pairs=2,
                           max_iterations=engine.MAX_ITERATIONS)
     st = engine.initial_state(cfg)
     res = st._res
     res.ensure_trace(200)
     a = res.run_args()
-    a.flags = RUN_FORCE | RUN_TIMING
+    a.flags = RUN_FORCE | RUN_TIMING | xflags
     a.gens_this_call = 40
     sp = torch.cuda.current_stream().cuda_stream
     check(lib.hga_run(a, sp), "run")
@@ -34,16 +37,23 @@ for m, N in ((12, 1000), (20, 10_000), (28, 31_250), (36, 312_500)):
     off = int(lib.hga_run_timing_offset(m))
     ts = res.run_ws[off:off + 64 * 20 * 8].view(torch.int64).view(64, 20).cpu().numpy().astype(np.float64)[:40]
     med = lambda x: float(np.median(x)) / 1e3
-    print(json.dumps({"m": m, "detail_us": {"B": med(ts[:, 1] - ts[:, 0]), "bar1": med(ts[:, 2] - ts[:, 1]),
+    print(json.dumps({"m": m, "one_barrier": bool(xflags), "detail_us": {"B": med(ts[:, 1] - ts[:, 0]), "bar1": med(ts[:, 2] - ts[:, 1]),
                                              "E_prefix": med(ts[:, 7] - ts[:, 2]), "E_tiles": med(ts[:, 8] - ts[:, 7]),
                                              "E_flush": med(ts[:, 9] - ts[:, 8]), "bar2": med(ts[:, 4] - ts[:, 9]),
                                              "F": med(ts[1:, 0] - ts[:-1, 4])},
                       "sm_mhz": float(np.median((ts[:, 11] - ts[:, 10]) / (ts[:, 4] - ts[:, 0]) * 1e3))}))
+    d = lambda a, b: med(ts[:, b] - ts[:, a])  # noqa: E731
+    print(json.dumps({"m": m, "fine_us": {
+        "B_tau": d(0, 3), "B_scan": d(3, 1), "E_prefix": d(2, 5), "E_init": d(5, 7),
+        "t_prepare": d(7, 12), "t_gather": d(12, 13), "t_copy": d(13, 14), "t_xover": d(14, 15),
+        "t_mutate": d(15, 16), "t_chain": d(16, 17), "t_fit": d(17, 18), "t_store": d(18, 19),
+        "t_rest": d(19, 8)}}))
     gen = np.diff(ts[:, 0])
-    print(json.dumps({"m": m, "N": N, "us_per_gen": float(np.median(gen)) / 1e3,
+    print(json.dumps({"m": m, "N": N, "one_barrier": bool(xflags), "us_per_gen": float(np.median(gen)) / 1e3,
                       "offspring_evals_per_s": 2 * N / (float(np.median(gen)) / 1e9)}), flush=True)
 
 # launch overhead: single-generation launches, plain vs CUDA-graph replay
+engine._RUN_FLAGS = 0
 for m, N in ((20, 10_000),):
     cfg = engine.GAConfig(order=m, population=N, seed=1, fitness="f2", mutation_cols=4, mutation_row_pairs=2,
                           max_iterations=engine.MAX_ITERATIONS)

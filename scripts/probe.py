@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -51,7 +52,7 @@ def probe_pipes():
 
 def probe_fitness(quick):
     st = torch.cuda.current_stream().cuda_stream
-    for m in (8, 12, 16, 20, 24, 28, 32, 36, 40, 48, 64, 96, 128):
+    for m in (8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 52, 56, 60, 64, 96, 128):
         n = 2_000_000 if m <= 32 else (1_000_000 if m <= 64 else 200_000)
         if quick:
             n //= 4
@@ -63,10 +64,15 @@ def probe_fitness(quick):
             if var == 15:
                 o = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(4)]
             ptrs = [x.data_ptr() if x is not None else None for x in o]
-            t = timed(lambda: lib.hga_fitness_i8(pop.data_ptr(), n, m, var, *ptrs, None, None, 0, st))
-            bytes_ = n * (m * m + 8 * bin(var).count("1"))
-            print(json.dumps({"kernel": "fitness_i8", "m": m, "n": n, "variant": name, "evals_per_s": n / t,
-                              "GBps": bytes_ / t / 1e9, "us": t * 1e6}), flush=True)
+            tc = m <= 64
+            for path in (("tcgen05", "popc") if tc else ("popc",)):
+                if tc:
+                    os.environ["HGA_FITNESS_TC"] = "0" if path == "popc" else "all"
+                t = timed(lambda: lib.hga_fitness_i8(pop.data_ptr(), n, m, var, *ptrs, None, None, 0, st))
+                os.environ.pop("HGA_FITNESS_TC", None)
+                bytes_ = n * (m * m + 8 * bin(var).count("1"))
+                print(json.dumps({"kernel": "fitness_i8", "path": path, "m": m, "n": n, "variant": name,
+                                  "evals_per_s": n / t, "GBps": bytes_ / t / 1e9, "us": t * 1e6}), flush=True)
         packed = engine._pack(pop)
         t = timed(lambda: lib.hga_fitness_packed(packed.data_ptr(), n, m, 2, None, outs.data_ptr(), None, None, st))
         W = (m + 31) // 32

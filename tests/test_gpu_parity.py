@@ -79,6 +79,43 @@ def test_fitness_rejects_non_sign(cuda_device):
         hga.evaluate(np.ones((2, 4, 4), np.int8), "f3")
 
 
+@pytest.mark.parametrize("m", [36, 40, 44, 48, 52, 56, 60, 64])
+def test_fitness_tensor_core_path_matches_popc_path(m, cuda_device, monkeypatch):
+    """Orders 36..64 run on tcgen05 (kind::i8 Gram in TMEM); HGA_FITNESS_TC=0
+    selects the XOR+POPC kernel.  Both must equal the oracle bit for bit,
+    for odd batch sizes (the last MMA pair half empty) and fixtures."""
+    rng = np.random.default_rng(m)
+    pops = [oracle.random_balanced(m, 2047, 5 + m, 1, 0, 0),
+            rng.choice(np.array([-1, 1], dtype=np.int8), size=(3, m, m)),
+            rng.choice(np.array([-1, 1], dtype=np.int8), size=(1, m, m))]
+    if m in (48, 64):
+        h = hga.sylvester(6)[:m, :m] if m == 64 else None
+        if h is not None:
+            pops.append(np.stack([h, -h, h.T]))
+    for pop in pops:
+        want = oracle.penalties(pop, threads=4)
+        got_tc = hga.penalties(pop)
+        monkeypatch.setenv("HGA_FITNESS_TC", "0")
+        got_pc = hga.penalties(pop)
+        monkeypatch.delenv("HGA_FITNESS_TC")
+        for col, key in enumerate(("f1", "f2", "orth", "sq")):
+            assert np.array_equal(got_tc[key], want[:, col]), (m, key, len(pop))
+            assert np.array_equal(got_pc[key], want[:, col]), (m, key, len(pop))
+        for key in ("f1", "f2"):
+            assert np.array_equal(hga.evaluate(pop, key), want[:, ("f1", "f2").index(key)])
+
+
+@pytest.mark.parametrize("m", [36, 48, 60, 64])
+def test_fitness_tensor_core_rejects_non_sign(m, cuda_device):
+    base = oracle.random_balanced(m, 5, 3, 1, 0, 0)
+    for (k, r, c, v) in ((0, 0, 0, 0), (4, m - 1, m - 1, 2), (2, m // 2, m - 1, -3), (3, 7, 17, 0)):
+        pop = base.copy()
+        pop[k, r, c] = v
+        with pytest.raises(ValueError):
+            hga.evaluate(pop, "f2")
+    assert np.array_equal(hga.evaluate(base, "f2"), oracle.evaluate(base, "f2"))
+
+
 def test_fitness_large_population_sampled(cuda_device):
     m, n = 20, 1_000_000
     pop_t = engine.init_population_device(engine.GAConfig(order=m, population=n // 4, seed=2024, rng="reference"))
@@ -311,6 +348,33 @@ def test_philox_stall_restart_runs(cuda_device):
     rec = hga.run_search(cfg)
     assert all(a >= b for a, b in zip(rec.trace, rec.trace[1:]))
     assert rec.best_fitness == rec.trace[-1] or rec.best_fitness <= rec.trace[-1]
+
+
+@pytest.mark.parametrize("m,N,fit,nc,nr,sw", [(20, 1000, "f2", 4, 2, None), (12, 300, "f1", 1, 2, 4),
+                                               (28, 2000, "f2", 2, 3, None), (36, 600, "f1", 3, 3, None),
+                                               (16, 100, "sq", 1, 1, 3), (8, 32768, "f2", 1, 2, None),
+                                               (64, 257, "f2", 5, 4, None)])
+def test_one_barrier_loop_matches_two_barrier(m, N, fit, nc, nr, sw, cuda_device, monkeypatch):
+    """The one-barrier generation loop (4N <= 131072) selects the same
+    survivors with the same ranks as the two-barrier loop: identical runs."""
+    from paper_2208_14961_b200._lib import RUN_ONE_BARRIER
+
+    out = []
+    for flags in (0, RUN_ONE_BARRIER):
+        monkeypatch.setattr(engine, "_RUN_FLAGS", flags)
+        cfg = engine.GAConfig(order=m, population=N, seed=9, fitness=fit, mutation_cols=nc, mutation_row_pairs=nr,
+                              stall_window=sw, max_iterations=400)
+        st = hga.initial_state(cfg)
+        engine._run_device(st, 60)
+        for _ in range(3):
+            if st.best_fitness == 0:
+                break
+            hga.step(st)
+        _invariants(st)
+        out.append((list(st.trace), st.population, st.fitness, st.best_matrix))
+    a, b = out
+    assert a[0] == b[0]
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
 
 
 def test_single_gpu_island_and_elites(cuda_device):
