@@ -157,7 +157,8 @@ def test_reference_streams(golden, cuda_device):
 
 
 def test_permutation_large_matches_oracle(cuda_device):
-    for n in (50_000, 60_000, 200_001):
+    # serial replay below 8192 entries, parallel replay (k_pfy_*) from 8192 on
+    for n in (8191, 8192, 8193, 20_000, 50_000, 60_000, 200_001):
         got = RngStream(11, 5, counter=3).permutation(n)
         assert np.array_equal(got, oracle.permutation(11, 5, 3, n)), n
 
