@@ -41,7 +41,11 @@ constexpr int kMaxStages = 48;
 constexpr int kB = 2;          // MMA pairs per pipeline unit (one barrier round trip per unit)
 constexpr int kSlotCols = kB * 64;
 constexpr int kSlots = 512 / kSlotCols;  // TMEM accumulator slots
-constexpr int kEpiGroups = 3;  // epilogue groups of 4 warps (one per TMEM lane quarter); group g takes pairs it = g mod 3
+// epilogue groups of 4 warps (one per TMEM lane quarter); group g takes units it = g mod kEpiGroups.
+// A group starts waiting on a slot's mbarrier only after finishing unit it - kEpiGroups, so the slot's
+// previous phase (unit it - kSlots) is complete iff kSlots >= kEpiGroups: parity waits stay unambiguous.
+constexpr int kEpiGroups = kSlots >= 3 ? 3 : kSlots;
+static_assert(kSlots >= kEpiGroups, "parity waits need kSlots >= kEpiGroups");
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kLoadWarps = 4;  // two per tile of the pair
 constexpr int kCheckWarps = kLoadWarps;  // check warp w re-reads what loader warp w copied
