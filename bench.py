@@ -330,7 +330,7 @@ def run_e2e(args, cfg, hga, engine, torch):
     return {"value": 2 * N_PAIRS / t, "unit": UNIT, "h2d_bytes_per_step": int(pop.nbytes + fit.nbytes + 64),
             "d2h_bytes_per_step": int(pop.nbytes + fit.nbytes + 8), "steps": steps, "ms_per_step": t * 1e3,
             "api": "paper_2208_14961_b200.engine.step(state) with numpy population/fitness (drop-in for "
-                   "hadamard_ga.step)"}
+                   "hadamard_ga.step; one hga_step_host call: H2D, pack, generation, chunked unpack + D2H)"}
 
 
 def run_fitness_sweep(args, engine, torch, lib, peak):

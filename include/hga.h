@@ -225,6 +225,26 @@ int hga_run_init(const hga_run_args *args, void *stream);
 int hga_run_prepare(const hga_run_args *args, void *stream);
 int hga_run(const hga_run_args *args, void *stream);
 
+/* One Philox generation on a HOST-resident state: the reference's
+ * step(state) (engine.py:449-469) when state.population / state.fitness are
+ * host (numpy) arrays that the caller owns and that are updated in place.
+ * host_pop (4N x m x m int8) and host_fit (4N int64) should be page-locked
+ * (cudaHostRegister) so the copies are DMA.  The population goes up on
+ * copy_stream in one piece and is packed on `stream`; the generation runs as
+ * hga_run(gens_this_call = 1, HGA_RUN_FORCE)
+ * from state_in (8 values: iteration, best, last restart, 0, 0, 0, 1, last
+ * trace value); the new population is unpacked and copied back piece by
+ * piece (`chunks` pieces, each copied as soon as it is unpacked) on
+ * copy_stream.  Orders 4..64 (m % 4 == 0); HGA_E_UNSUPPORTED otherwise.
+ * dev_i8 is a device int8 staging buffer of 4N*m*m
+ * bytes.  On return (copy_stream synchronised) host_pop/host_fit hold the new
+ * population, state_out[0..7] the device state after the generation and
+ * *flag_out the HGA_FLAG_* bits (HGA_FLAG_NOT_SIGN: an input entry was not
+ * +-1). */
+int hga_step_host(const hga_run_args *args, int8_t *host_pop, int64_t *host_fit, int8_t *dev_i8,
+                  const int64_t *state_in, int64_t *state_out, int32_t *flag_out, int32_t chunks,
+                  void *stream, void *copy_stream);
+
 #ifdef __cplusplus
 }
 #endif

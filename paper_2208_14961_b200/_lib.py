@@ -99,6 +99,7 @@ SIGNATURES = {
     "hga_run_init": (_int, [ctypes.POINTER(RunArgs), _vp]),
     "hga_run_prepare": (_int, [ctypes.POINTER(RunArgs), _vp]),
     "hga_run": (_int, [ctypes.POINTER(RunArgs), _vp]),
+    "hga_step_host": (_int, [ctypes.POINTER(RunArgs), _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int32, _vp, _vp]),
 }
 
 

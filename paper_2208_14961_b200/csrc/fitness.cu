@@ -243,6 +243,66 @@ __global__ void k_unpack(const uint32_t* __restrict__ cols, int64_t n, int m, in
     }
 }
 
+// Pack for m % 4 == 0, m <= 64: thread (matrix k, column quad jq) walks the
+// rows with one 4-byte load each (consecutive threads read consecutive
+// quads of a row), collects the four columns' sign bits and checks the bytes
+// are +-1 (byte ^ 1 has bit 0 clear and bits 1..7 equal).
+template <int W>
+__global__ void k_pack_quads(const int8_t* __restrict__ pop, int64_t n, int m, uint32_t* __restrict__ cols,
+                             int32_t* bad_flag) {
+    const int q4 = m >> 2;
+    const int64_t quads = n * q4;
+    uint32_t bad = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < quads; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t / q4;
+        const int jq = (int)(t - k * q4);
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(pop + k * m * (int64_t)m) + jq;
+        uint32_t w[4][W];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int x = 0; x < W; ++x) w[c][x] = 0;
+        for (int r = 0; r < m; ++r) {
+            const uint32_t v = __ldg(p + r * q4);
+            const uint32_t a8 = v ^ 0x01010101u, b8 = a8 & 0xFEFEFEFEu;
+            bad |= (a8 & 0x01010101u) | ((b8 ^ (b8 << 1)) & 0xFCFCFCFCu);
+#pragma unroll
+            for (int x = 0; x < W; ++x) {
+                if ((r >> 5) != x) continue;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) w[c][x] |= ((v >> (8 * c + 7)) & 1u) << (r & 31);
+            }
+        }
+        uint32_t* out = cols + (k * m + 4 * jq) * W;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int x = 0; x < W; ++x) out[c * W + x] = w[c][x];
+    }
+    if (bad && bad_flag) atomicOr(bad_flag, HGA_FLAG_NOT_SIGN);
+}
+
+// Row-at-a-time unpack for m % 4 == 0: thread (matrix k, row r) reads row
+// r's bit from each column word (neighbouring rows share the words through
+// L1) and writes the row as m / 4 four-byte stores.
+__global__ void k_unpack_rows(const uint32_t* __restrict__ cols, int64_t n, int m, int W,
+                              int8_t* __restrict__ pop) {
+    const int64_t rows = n * m;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t / m;
+        const int r = (int)(t - k * m);
+        const uint32_t* c = cols + k * m * W + (r >> 5);
+        const int sh = r & 31;
+        uint32_t* out = reinterpret_cast<uint32_t*>(pop + t * m);
+        for (int j = 0; j < m; j += 4) {
+            uint32_t w = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w |= (((__ldg(c + (j + q) * W) >> sh) & 1u) ? 0xFFu : 0x01u) << (8 * q);
+            out[j >> 2] = w;
+        }
+    }
+}
+
 // -------------------------------------------------------------- host side
 
 static int g_sm_count[16] = {0};
@@ -377,14 +437,24 @@ int hga_pack_i8(const int8_t* pop, int64_t n, int32_t m, uint32_t* cols, int32_t
     if (n < 0 || m < 1 || m > 4096) return HGA_E_INVALID;
     if (n == 0) return HGA_OK;
     const int W = words_for(m);
-    k_pack_any<<<grid_for(n * m * W, 256), 256, 0, (cudaStream_t)stream>>>(pop, n, m, W, cols, bad_flag);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (m % 4 == 0 && m <= 64 && (((uintptr_t)pop) & 3) == 0) {
+        const unsigned g = grid_for(n * (int64_t)(m / 4), 256);
+        if (W == 1) k_pack_quads<1><<<g, 256, 0, st>>>(pop, n, m, cols, bad_flag);
+        else k_pack_quads<2><<<g, 256, 0, st>>>(pop, n, m, cols, bad_flag);
+    } else {
+        k_pack_any<<<grid_for(n * m * W, 256), 256, 0, st>>>(pop, n, m, W, cols, bad_flag);
+    }
     return to_rc(cudaGetLastError());
 }
 
 int hga_unpack_i8(const uint32_t* cols, int64_t n, int32_t m, int8_t* pop, void* stream) {
     if (n < 0 || m < 1 || m > 4096) return HGA_E_INVALID;
     if (n == 0) return HGA_OK;
-    k_unpack<<<grid_for(n * m * (int64_t)m, 256), 256, 0, (cudaStream_t)stream>>>(cols, n, m, words_for(m), pop);
+    if (m % 4 == 0 && (((uintptr_t)pop) & 3) == 0)
+        k_unpack_rows<<<grid_for(n * (int64_t)m, 256), 256, 0, (cudaStream_t)stream>>>(cols, n, m, words_for(m), pop);
+    else
+        k_unpack<<<grid_for(n * m * (int64_t)m, 256), 256, 0, (cudaStream_t)stream>>>(cols, n, m, words_for(m), pop);
     return to_rc(cudaGetLastError());
 }
 

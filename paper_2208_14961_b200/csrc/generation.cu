@@ -18,6 +18,10 @@
 //         parents copied to the new buffer (out-of-place gather, engine.py:247)
 //      F  trace / best / stop / stall-restart bookkeeping, replicated in every
 //         CTA from the same global values so all CTAs agree without a barrier
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "generation.cuh"
 #include "run_common.cuh"
 #include "run_v2.cuh"
@@ -668,6 +672,15 @@ static int run2_prepare(const hga_run_args* a, cudaStream_t st) {
 
 }  // namespace hga
 
+namespace hga {
+// state block of a host-driven step: iteration, best, last restart, parity 0,
+// best index 0, stop 0, run length, last trace value
+__global__ void k_set_state(int64_t* s, int64_t it, int64_t best, int64_t last_restart, int64_t run, int64_t last) {
+    const int64_t v[8] = {it, best, last_restart, 0, 0, 0, run, last};
+    if (threadIdx.x < 8) s[threadIdx.x] = v[threadIdx.x];
+}
+}  // namespace hga
+
 using namespace hga;
 
 static bool valid_var(uint32_t v) { return v == HGA_VAR_F1 || v == HGA_VAR_F2 || v == HGA_VAR_SQ; }
@@ -755,6 +768,84 @@ int hga_run_init(const hga_run_args* a, void* stream) {
     if (rc) return rc;
     if (run2_supported(a)) return run2_prepare(a, st);
     return HGA_OK;
+}
+
+int hga_step_host(const hga_run_args* a, int8_t* host_pop, int64_t* host_fit, int8_t* dev_i8,
+                  const int64_t* state_in, int64_t* state_out, int32_t* flag_out, int32_t chunks, void* stream,
+                  void* copy_stream) {
+    if (!run_args_ok(a) || !host_pop || !host_fit || !dev_i8 || !state_in || !state_out || !flag_out || chunks < 1)
+        return HGA_E_INVALID;
+    if (!run2_supported(a)) return HGA_E_UNSUPPORTED;  // orders > 64 keep the torch-side path
+    cudaStream_t st = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
+    const int m = a->m, W = words_for(m);
+    const int64_t total = 4 * a->n_pairs, mm = (int64_t)m * m, mw = (int64_t)m * W;
+    const int k = (int)std::min<int64_t>(chunks, total);
+    int32_t* dflag = &reinterpret_cast<RunWs2*>(a->ws)->host_flag;
+    // events: one per download piece plus three stream joins; kept in a per-thread
+    // pool (creating ~20 events per call costs tens of microseconds)
+    thread_local std::vector<cudaEvent_t> pool;
+    while ((int)pool.size() < 2 * k + 3) {
+        cudaEvent_t ne;
+        const cudaError_t ce = cudaEventCreateWithFlags(&ne, cudaEventDisableTiming);
+        if (ce != cudaSuccess) return to_rc(ce);
+        pool.push_back(ne);
+    }
+    cudaEvent_t* ev = pool.data();
+    auto done = [](int rc) { return rc; };
+    // HGA_STEP_TIMING=1: print the stream timeline of this call (diagnostics)
+    const bool tm = std::getenv("HGA_STEP_TIMING") != nullptr;
+    cudaEvent_t te[6];
+    if (tm)
+        for (auto& t : te) cudaEventCreate(&t);
+    if (tm) cudaEventRecord(te[0], st);
+    cudaError_t e = cudaEventRecord(ev[2 * k], st);  // the staging buffers are free once prior work is done
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[2 * k], 0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int32_t), st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(a->fit[0], host_fit, total * sizeof(int64_t), cudaMemcpyHostToDevice, cs);
+    // upload in one piece (splitting it costs more than the ~12 us of packing it would hide)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dev_i8, host_pop, total * mm, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[0], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[0], 0);
+    if (e == cudaSuccess) {
+        const int rc = hga_pack_i8(dev_i8, total, m, a->pop[0], dflag, st);
+        if (rc) return done(rc);
+    }
+    if (e != cudaSuccess) return done(to_rc(e));
+    if (tm) cudaEventRecord(te[1], cs);
+    if (tm) cudaEventRecord(te[2], st);
+    k_set_state<<<1, 8, 0, st>>>(a->state, state_in[0], state_in[1], state_in[2], state_in[6], state_in[7]);
+    hga_run_args r = *a;
+    r.gens_this_call = 1;
+    r.flags |= HGA_RUN_FORCE;  // exactly one generation: the new population is in buffer 1
+    int rc = hga_run_prepare(&r, st);
+    if (!rc) rc = hga_run(&r, st);
+    if (rc) return done(rc);
+    if (tm) cudaEventRecord(te[3], st);
+    for (int i = 0; i < k && e == cudaSuccess; ++i) {
+        const int64_t lo = total * i / k, hi = total * (i + 1) / k;
+        rc = hga_unpack_i8(a->pop[1] + lo * mw, hi - lo, m, dev_i8 + lo * mm, st);
+        if (rc) return done(rc);
+        e = cudaEventRecord(ev[k + i], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[k + i], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(host_pop + lo * mm, dev_i8 + lo * mm, (hi - lo) * mm, cudaMemcpyDeviceToHost, cs);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(ev[2 * k + 1], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[2 * k + 1], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host_fit, a->fit[1], total * sizeof(int64_t), cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(state_out, a->state, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(flag_out, dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
+    if (tm) cudaEventRecord(te[4], st);
+    if (tm) cudaEventRecord(te[5], cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (tm) {
+        float ms[5];
+        for (int i = 1; i < 6; ++i) cudaEventElapsedTime(&ms[i - 1], te[0], te[i]);
+        std::fprintf(stderr, "hga_step_host us: h2d_done %.1f packs_done %.1f run_done %.1f unpacks_done %.1f d2h_done %.1f\n",
+                     ms[0] * 1e3, ms[1] * 1e3, ms[2] * 1e3, ms[3] * 1e3, ms[4] * 1e3);
+        for (auto& t : te) cudaEventDestroy(t);
+    }
+    return done(to_rc(e));
 }
 
 int hga_philox_init_packed(uint64_t seed, uint64_t purpose, uint64_t generation, int64_t first_slot,

@@ -46,6 +46,7 @@ struct RunWs2 {
     unsigned long long best_key[3];
     unsigned long long par_key[3];
     unsigned long long restart_key;
+    int32_t host_flag;  // hga_step_host: HGA_FLAG_* of the uploaded population
     uint32_t kmin[3];
     uint32_t kmax[3];
     uint32_t cnt_lt[kR2MaxGrid];
@@ -774,6 +775,8 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     const bool timing_blk = (A.flags & HGA_RUN_TIMING) != 0 && bid == 0;
     uint32_t next_kmin = 0, next_kmax = 0;
     bool have_krange = false;
+    int64_t fpre[kSelItems];  // first batch of the select scan's fitness values, prefetched after barrier 2
+    bool have_fpre = false;
 
     for (int64_t gi = 0; gi < A.gens_this_call && !stop; ++gi) {
         const int64_t gen = iter + 1;
@@ -852,8 +855,8 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
         } else {
             // ---- B: threshold, tie quota, local survivor lists
             // first batch of fitness values: independent of tau, so load it under the histogram scan
-            int64_t fpre[kSelItems];
-            if (wid < pw_sel) load_items(f_old, lo + (int64_t)tid * kSelItems, hi, fpre);
+            if (!have_fpre && wid < pw_sel) load_items(f_old, lo + (int64_t)tid * kSelItems, hi, fpre);
+            have_fpre = false;
             if (!have_krange) {  // otherwise read with the bookkeeping loads of the previous generation
                 next_kmin = __ldcg(&ws->kmin[rslot]);
                 next_kmax = __ldcg(&ws->kmax[rslot]);
@@ -1021,6 +1024,10 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
 
         // ---- F: bookkeeping (identical in every CTA)
         {
+            if (!ONE && wid < pw_sel) {  // next generation's first select batch, under the bookkeeping loads
+                load_items(f_new, lo + (int64_t)tid * kSelItems, hi, fpre);
+                have_fpre = true;
+            }
             const unsigned long long key = __ldcg(&ws->best_key[bslot]);
             next_kmin = __ldcg(&ws->kmin[hslot]);  // key range of the next generation's histogram
             next_kmax = __ldcg(&ws->kmax[hslot]);
@@ -1117,6 +1124,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
                     }
                 }
                 last_restart = iter;
+                have_fpre = false;  // offspring fitness was rewritten
                 grid_sync(&ws->bar);
                 if (bid == 0 && tid == 0) ws->restart_key = ~0ull;
                 stop = best == 0;

@@ -27,7 +27,9 @@ orthogonal column pairs), and `penalties` returns all four from one pass.
 
 from __future__ import annotations
 
+import ctypes
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -706,19 +708,56 @@ class _HostBridge:
         self.res = _Resident(self.cfg, int(state.seed) & MASK64)
         m, total = self.cfg.order, self.cfg.total
         self.pop_i8 = torch.empty((total, m, m), dtype=torch.int8, device=self.res.dev)
-        self.registered = []
+        # page-locked host arrays (address -> array, kept alive while registered);
+        # unregistered when the bridge (i.e. the host state) goes away
+        self.registered: dict[int, np.ndarray] = {}
+        self._finalizer = weakref.finalize(self, _unregister_all, self.registered)
         self.inner = SearchState(self.cfg, int(state.seed) & MASK64, self.res, 0, 0, [], None)
+        self.copy_stream = torch.cuda.Stream(device=self.res.dev)
+        self.host_state = torch.empty(8, dtype=torch.int64, pin_memory=True)
+        self.host_state_in = torch.empty(8, dtype=torch.int64, pin_memory=True)  # pinned: no hidden stream sync
+        self.host_flag = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self.args = None
 
     def pin(self, arr: np.ndarray) -> None:
-        key = (arr.ctypes.data, arr.nbytes)
-        if key in self.registered or arr.nbytes == 0:
+        held = self.registered.get(arr.ctypes.data)
+        if arr.nbytes == 0 or (held is not None and held.nbytes >= arr.nbytes):
             return
-        rc = torch.cuda.cudart().cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+        rt = torch.cuda.cudart()
+        rc = rt.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
         if int(rc) == 0:
-            self.registered.append(key)
+            self.registered[arr.ctypes.data] = arr
+        else:
+            rt.cudaGetLastError()  # not fatal: the copies go through pageable staging instead
+
+
+def _unregister_all(registered: dict) -> None:
+    try:
+        rt = torch.cuda.cudart()
+        for addr in list(registered):
+            rt.cudaHostUnregister(addr)
+        rt.cudaGetLastError()
+    except Exception:  # noqa: BLE001 -- interpreter shutdown
+        pass
+    registered.clear()
+
+
+_HOST_CHUNKS = 8  # host <-> device population copies are pipelined against pack / unpack in this many pieces
+
+
+def _chunks(total: int) -> list[tuple[int, int]]:
+    k = max(1, min(_HOST_CHUNKS, total))
+    return [(total * i // k, total * (i + 1) // k) for i in range(k)]
 
 
 def _step_host(state):
+    """One generation on a host (numpy) state, in place (engine.py:449-469).
+
+    The int8 population goes up and comes back every step (the caller owns
+    the arrays); the copies run on a side stream in chunks, each chunk packed
+    (unpacked) on the compute stream as soon as it has landed (before it
+    leaves), and in Philox mode the only host synchronisation is the final one.
+    """
     bridge = getattr(state, "_hga_bridge", None)
     if bridge is None:
         bridge = _HostBridge(state)
@@ -730,32 +769,85 @@ def _step_host(state):
     bridge.pin(fit_np)
     res, inner = bridge.res, bridge.inner
     res.cur = cur = 0  # the host arrays are authoritative: upload into buffer 0
-    bridge.pop_i8.copy_(torch.from_numpy(pop_np), non_blocking=True)
-    res.fit[cur].copy_(torch.from_numpy(fit_np), non_blocking=True)
+    it0, best0 = int(state.iteration), int(state.best_fitness)
+    last0 = int(state.trace[-1]) if state.trace else best0
+    if bridge.cfg.rng == "philox" and res.m <= 64:
+        # the whole step is enqueued natively (hga_step_host): chunked copies on a
+        # side stream overlapped with pack / unpack, one synchronisation at the end
+        if bridge.args is None:  # the trace buffer is not used by this path; args stay valid
+            bridge.args = res.run_args()
+            bridge.st_in = (ctypes.c_int64 * 8)()
+            bridge.hs_np, bridge.hf_np = bridge.host_state.numpy(), bridge.host_flag.numpy()
+        st_in = bridge.st_in
+        st_in[0], st_in[1], st_in[2], st_in[6], st_in[7] = it0, best0, 0, 1, last0
+        check(lib.hga_step_host(bridge.args, pop_np.ctypes.data, fit_np.ctypes.data, bridge.pop_i8.data_ptr(), st_in,
+                                bridge.host_state.data_ptr(), bridge.host_flag.data_ptr(), _HOST_CHUNKS,
+                                stream_ptr(), bridge.copy_stream.cuda_stream), "hga_step_host")
+        res.cur = 1
+        if int(bridge.hf_np[0]) & FLAG_NOT_SIGN:
+            raise ValueError("step: matrix entries must be +1 or -1")
+        _finish_host_step(state, pop_np, fit_np, int(bridge.hs_np[0]), int(bridge.hs_np[7]))
+        return state
     flag = _dev.new_flag()
-    m, total = res.m, 4 * res.N
-    check(lib.hga_pack_i8(bridge.pop_i8.data_ptr(), total, m, res.pop[cur].data_ptr(), flag.data_ptr(),
-                          stream_ptr()), "hga_pack_i8")
-    inner.iteration, inner.best_fitness = int(state.iteration), int(state.best_fitness)
-    inner.trace = [int(state.trace[-1])] if state.trace else [int(state.best_fitness)]
-    res.dstate.copy_(torch.tensor([inner.iteration, inner.best_fitness, 0, cur, 0, 0, 1, inner.trace[-1]],
-                                  dtype=torch.int64), non_blocking=True)
-    inner.best_matrix = None
-    check(lib.hga_run_prepare(res.run_args(), stream_ptr()), "hga_run_prepare") if bridge.cfg.rng == "philox" else None
-    step(inner)
-    check(lib.hga_unpack_i8(res.pop[res.cur].data_ptr(), total, m, bridge.pop_i8.data_ptr(), stream_ptr()),
-          "hga_unpack_i8")
-    torch.from_numpy(pop_np).copy_(bridge.pop_i8, non_blocking=True)
-    torch.from_numpy(fit_np).copy_(res.fit[res.cur], non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    m, total, mw = res.m, 4 * res.N, res.mw
+    comp, cs = torch.cuda.current_stream(), bridge.copy_stream
+    pop_t, fit_t = torch.from_numpy(pop_np), torch.from_numpy(fit_np)
+    parts = _chunks(total)
+    cs.wait_stream(comp)
+    with torch.cuda.stream(cs):
+        res.fit[cur].copy_(fit_t, non_blocking=True)
+    for a, b in parts:
+        with torch.cuda.stream(cs):
+            bridge.pop_i8[a:b].copy_(pop_t[a:b], non_blocking=True)
+            landed = torch.cuda.Event()
+            landed.record(cs)
+        comp.wait_event(landed)
+        check(lib.hga_pack_i8(bridge.pop_i8[a].data_ptr(), b - a, m, res.pop[cur][a * mw].data_ptr(),
+                              flag.data_ptr(), comp.cuda_stream), "hga_pack_i8")
+    comp.wait_stream(cs)
+    bridge.host_state_in.copy_(torch.tensor([it0, best0, 0, cur, 0, 0, 1, last0], dtype=torch.int64))
+    res.dstate.copy_(bridge.host_state_in, non_blocking=True)
+    if bridge.cfg.rng == "philox":
+        check(lib.hga_run_prepare(res.run_args(), stream_ptr()), "hga_run_prepare")
+        res.ensure_trace(it0 + 1)
+        args = res.run_args()
+        args.gens_this_call = 1
+        args.flags |= RUN_FORCE  # exactly one generation: the new population is in buffer cur ^ 1
+        check(lib.hga_run(args, stream_ptr()), "hga_run")
+        new = cur ^ 1
+    else:
+        inner.iteration, inner.best_fitness, inner.trace, inner.best_matrix = it0, best0, [last0], None
+        step(inner)
+        new = res.cur
+    for a, b in parts:
+        check(lib.hga_unpack_i8(res.pop[new][a * mw].data_ptr(), b - a, m, bridge.pop_i8[a].data_ptr(),
+                                comp.cuda_stream), "hga_unpack_i8")
+        ready = torch.cuda.Event()
+        ready.record(comp)
+        cs.wait_event(ready)
+        with torch.cuda.stream(cs):
+            pop_t[a:b].copy_(bridge.pop_i8[a:b], non_blocking=True)
+    cs.wait_stream(comp)
+    with torch.cuda.stream(cs):
+        fit_t.copy_(res.fit[new], non_blocking=True)
+        bridge.host_state.copy_(res.dstate, non_blocking=True)
+    cs.synchronize()
     _check_flag(flag, "step")
-    fmin = inner.trace[-1]
-    state.iteration = inner.iteration
+    if bridge.cfg.rng == "philox":
+        it1, fmin = int(bridge.host_state[0]), int(bridge.host_state[7])
+    else:
+        it1, fmin = inner.iteration, inner.trace[-1]
+    _finish_host_step(state, pop_np, fit_np, it1, fmin)
+    return state
+
+
+def _finish_host_step(state, pop_np: np.ndarray, fit_np: np.ndarray, it1: int, fmin: int) -> None:
+    """Trace / best bookkeeping of a host state (engine.py:430-437)."""
+    state.iteration = it1
     state.trace.append(fmin)
     if fmin < state.best_fitness:
         state.best_fitness = fmin
         state.best_matrix = pop_np[int(np.argmin(fit_np))].copy()
-    return state
 
 
 def _check_state(state: SearchState) -> None:

@@ -280,6 +280,56 @@ def test_reference_mode_run_records(golden, cuda_device):
         assert np.array_equal(rec.best_matrix, golden[f"run{i}_best"]), i
 
 
+# ------------------------------------------------------------------ drop-in step on host (numpy) states
+
+
+def _host_state(cfg, seed, pop, fit, best_matrix, best):
+    from dataclasses import dataclass, field
+
+    @dataclass
+    class HostState:  # field-for-field the reference's SearchState (engine.py:376-387)
+        config: object
+        seed: int
+        population: np.ndarray
+        fitness: np.ndarray
+        iteration: int
+        best_matrix: np.ndarray
+        best_fitness: int
+        trace: list = field(default_factory=list)
+
+    return HostState(cfg, seed, pop, fit, 0, best_matrix, best, [best])
+
+
+def test_host_state_step_reference_streams(golden, cuda_device):
+    """engine.step on numpy arrays (chunked copies + pack/unpack around the
+    generation) reproduces the reference's own state after three steps."""
+    for i in (0, 2, 5):
+        kw = run_config(golden, i)
+        cfg = engine.GAConfig(**kw, rng="reference")
+        o = oracle.initial_state(cfg.order, cfg.population, kw["seed"], cfg.fitness, cfg.mutation_cols,
+                                 cfg.mutation_row_pairs, cfg.mutation)
+        hs = _host_state(cfg, kw["seed"], o.population, o.fitness, o.best_matrix, o.best_fitness)
+        for _ in range(min(3, kw["max_iterations"])):
+            hga.step(hs)
+        assert np.array_equal(hs.population, golden[f"run{i}_state3_pop"]), i
+        assert np.array_equal(hs.fitness, golden[f"run{i}_state3_fit"]), i
+        assert hs.trace == golden[f"run{i}_trace"].tolist()[:len(hs.trace)], i
+
+
+def test_host_state_step_philox_matches_device_state(cuda_device):
+    for m, N in ((20, 1000), (12, 37), (36, 301)):
+        cfg = engine.GAConfig(order=m, population=N, seed=21, fitness="f2", mutation_cols=2, mutation_row_pairs=3)
+        dev = hga.initial_state(cfg)
+        hs = _host_state(cfg, dev.seed, dev.population.copy(), dev.fitness.copy(), dev.best_matrix.copy(),
+                         dev.best_fitness)
+        for _ in range(4):
+            hga.step(dev)
+            hga.step(hs)
+            assert np.array_equal(hs.population, dev.population), m
+            assert np.array_equal(hs.fitness, dev.fitness), m
+        assert hs.trace == dev.trace and hs.iteration == dev.iteration == 4
+
+
 # ------------------------------------------------------------------ production (Philox) loop
 
 
