@@ -394,6 +394,24 @@ def test_philox_search_finds_and_verifies(cuda_device):
     assert wins >= 1
 
 
+def test_philox_stochastic_parity_order12(cuda_device):
+    """Stochastic parity: the reference solves m = 12, N = 1000,
+    NC = 1, NR = 2, F1 in 30/30 seeds with a mean of 89.9 generations (range
+    53-125).  The Philox loop draws different random numbers but must show
+    the same behaviour; its seeds are fixed, so the check is deterministic.
+    (rng="reference" reproduces the reference's 30 runs exactly:
+    profiles/r01_stochastic_parity.jsonl.)"""
+    its = []
+    for sd in range(30):
+        rec = hga.run_search(engine.GAConfig(order=12, population=1000, max_iterations=3000, mutation_cols=1,
+                                             mutation_row_pairs=2, fitness="f1", seed=sd))
+        assert rec.success, sd
+        _check_solution(rec)
+        its.append(rec.iterations)
+    mean = sum(its) / len(its)
+    assert 70 <= mean <= 115, mean  # reference 89.9; the standard error of a 30-run mean is ~4
+
+
 def test_philox_stall_restart_runs(cuda_device):
     cfg = engine.GAConfig(order=16, population=50, seed=2, fitness="f2", max_iterations=300, stall_window=5)
     rec = hga.run_search(cfg)
