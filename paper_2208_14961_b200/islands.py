@@ -30,7 +30,8 @@ from ._dev import check, lib, stream_ptr
 from .engine import GAConfig, initial_state, _run_device, _best_from_packed
 from .rand import MASK64, mix64
 
-__all__ = ["IslandConfig", "Exchange", "GpuIsland", "IslandRecord", "island_seed", "run_islands"]
+__all__ = ["IslandConfig", "Exchange", "GpuIsland", "IslandRecord", "island_seed", "run_islands",
+           "shard_bounds", "evaluate_sharded"]
 
 
 @dataclass(frozen=True)
@@ -231,3 +232,45 @@ def run_islands(config: GAConfig, island_config: IslandConfig = IslandConfig(), 
                         complete=complete, iterations=island.iteration, best_fitness=best, best_matrix=best_matrix,
                         winner_rank=owner, wall_seconds=time.perf_counter() - start, migrations=migrations,
                         trace=trace)
+
+
+# ---------------------------------------------------------------- fitness-only sharding
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous slice [lo, hi) of n matrices owned by `rank` (SURVEY.md §8e:
+    matrices are independent units; sizes differ by at most one)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def evaluate_sharded(population, fitness: str = "f2", group=None, evaluator=None):
+    """`evaluate` across all ranks of a torch.distributed job: rank r scores
+    its contiguous slice on its own GPU and one all_gather returns the whole
+    fitness vector (int64, numpy) on every rank; no other collective.
+
+    Every rank passes the same population (numpy or a tensor); `evaluator`
+    replaces the GPU kernel (tests run the protocol on gloo with the CPU
+    oracle).  Without an initialised process group this is `evaluate`.
+    """
+    from . import engine
+
+    evaluator = evaluator or (lambda pop, fit: np.asarray(engine.evaluate(pop, fit)))
+    if not (dist.is_available() and dist.is_initialized()):
+        return evaluator(population, fitness)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = int(population.shape[0])
+    lo, hi = shard_bounds(n, world, rank)
+    mine = evaluator(population[lo:hi], fitness)
+    mine = torch.as_tensor(np.asarray(mine, dtype=np.int64))
+    width = -(-n // world)  # all_gather needs equal sizes: pad every slice to the largest
+    buf = torch.zeros(width, dtype=torch.int64)
+    buf[: hi - lo] = mine
+    if dist.get_backend(group) == "nccl":
+        buf = buf.cuda()
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    out = np.empty(n, dtype=np.int64)
+    for r, part in enumerate(parts):
+        a, b = shard_bounds(n, world, r)
+        out[a:b] = part[: b - a].cpu().numpy()
+    return out

@@ -446,6 +446,13 @@ def test_one_barrier_loop_matches_two_barrier(m, N, fit, nc, nr, sw, cuda_device
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
 
 
+def test_evaluate_sharded_single_process(cuda_device):
+    from paper_2208_14961_b200.islands import evaluate_sharded
+
+    pop = oracle.random_balanced(28, 777, 4, 1, 0, 0)
+    assert np.array_equal(evaluate_sharded(pop, "f2"), oracle.evaluate(pop, "f2"))
+
+
 def test_single_gpu_island_and_elites(cuda_device):
     from paper_2208_14961_b200.islands import GpuIsland, IslandConfig, run_islands
 

@@ -152,3 +152,49 @@ def test_payload_roundtrip():
     assert torch.equal(r2, rec) and torch.equal(f2, fit)
     pop = np.random.default_rng(0).choice(np.array([-1, 1], np.int8), size=(4, 36, 36))
     assert np.array_equal(unpack_np(pack_np(pop), 36), pop)
+
+
+def _shard_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, str(ROOT))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2208_14961_b200.islands import evaluate_sharded, shard_bounds
+
+        pop = oracle.init_population(12, 251, 3)  # 1004 matrices: not divisible by 3
+        seen = []
+
+        def ev(p, fit):
+            seen.append(len(p))
+            return oracle.evaluate(p, fit)
+
+        got = evaluate_sharded(pop, "f1", evaluator=ev)
+        q.put((rank, got.tolist(), seen, shard_bounds(len(pop), world, rank)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_fitness_gloo():
+    """Fitness-only sharding: each rank scores only its slice,
+    one all_gather returns the full, reference-equal vector on every rank."""
+    import oracle
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = oracle.evaluate(oracle.init_population(12, 251, 3), "f1").tolist()
+    bounds = []
+    for rank, got, seen, (lo, hi) in res:
+        assert got == want, rank
+        assert seen == [hi - lo]
+        bounds.append((lo, hi))
+    assert bounds == [(0, 334), (334, 669), (669, 1004)]
