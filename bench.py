@@ -218,7 +218,9 @@ def run_ours(args, rank, world, local_rank):
     prof = ROOT / "profiles" / "r01_k_run_traffic.json"
     if prof.exists():
         try:
-            roofline["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            t = json.loads(prof.read_text())
+            roofline["traffic"] = t.get("dram_bytes_per_launch",
+                                        (t.get("dram_bytes_read") or 0) + (t.get("dram_bytes_write") or 0) or None)
         except (ValueError, OSError):
             pass
 
