@@ -568,19 +568,25 @@ __device__ __forceinline__ void tile_compute(const TileCtx& C, TileShared& S, ui
             if (!first) continue;
             int reps = 1;
             for (int j2 = jc + 1; j2 < nc; ++j2) reps += pl[j2] == col;
+            // the column's words live in registers for the whole row-pair sequence:
+            // one shared-memory load and store per word instead of a
+            // read-modify-write per swap
             uint32_t* cw = row + col * W;
+            uint32_t w0 = cw[0], w1 = W > 1 ? cw[W > 1 ? 1 : 0] : 0u;
             for (int rep = 0; rep < reps; ++rep) {
                 for (int ir = 0; ir < nr; ++ir) {
                     const int ra = pl[nc + ir], rb = pl[nc + nr + ir];
-                    uint32_t* wa = cw + (ra >> 5);
-                    uint32_t* wb = cw + (rb >> 5);
-                    const uint32_t xa = (*wa >> (ra & 31)) & 1u, xb = (*wb >> (rb & 31)) & 1u;
-                    if (xa != xb) {
-                        *wa ^= 1u << (ra & 31);
-                        *wb ^= 1u << (rb & 31);
-                    }
+                    const uint32_t va = (W > 1 && (ra >> 5)) ? w1 : w0, vb = (W > 1 && (rb >> 5)) ? w1 : w0;
+                    const uint32_t flip = ((va >> (ra & 31)) ^ (vb >> (rb & 31))) & 1u;  // rows differ: swap
+                    const uint32_t ma = flip << (ra & 31), mb = flip << (rb & 31);
+                    if (W > 1 && (ra >> 5)) w1 ^= ma;
+                    else w0 ^= ma;
+                    if (W > 1 && (rb >> 5)) w1 ^= mb;
+                    else w0 ^= mb;
                 }
             }
+            cw[0] = w0;
+            if constexpr (W > 1) cw[1] = w1;
         }
     }
     group_sync(g);
