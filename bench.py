@@ -360,9 +360,9 @@ def run_fitness_sweep(args, engine, torch, lib, peak):
         popc_ceiling = 4.52e12 / ((m * (m - 1) // 2) * ((m + 31) // 32))
         hbm_ceiling = peak * 1e9 / (m * m + 8)
         ev = n / t
-        # orders >= 44 run the Gram on tcgen05 (kind::i8): the tensor work per
+        # orders >= 48 run the Gram on tcgen05 (kind::i8): the tensor work per
         # matrix is far below the HBM time, so HBM is that path's ceiling
-        tc = 44 <= m <= 64
+        tc = 48 <= m <= 64
         ceiling = hbm_ceiling if tc else min(popc_ceiling, hbm_ceiling)
         rows.append({"m": m, "n": n, "path": "tcgen05 kind::i8" if tc else "XOR+POPC",
                      "evals_per_s": ev, "GBps": bytes_ / t / 1e9, "hbm_frac": bytes_ / t / 1e9 / peak,

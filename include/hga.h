@@ -77,7 +77,7 @@ int hga_sm_count(int device);
  * NULL; `variants` selects which are computed (fused in one pass, the Gram
  * matrix never leaves the SM).  bad_flag (nullable) gets HGA_FLAG_NOT_SIGN
  * OR-ed in when an entry is not +-1.  ws is needed only for m > 128
- * (hga_fitness_i8_ws_bytes).  Orders 36..64 (16-byte aligned pop) run the
+ * (hga_fitness_i8_ws_bytes).  Orders 48..64 (16-byte aligned pop) run the
  * Gram on the tensor cores (tcgen05.mma.kind::i8, accumulators in TMEM);
  * the others, or HGA_FITNESS_TC=0 in the environment, the XOR+POPC kernels.
  * Results are identical. */

@@ -79,10 +79,11 @@ def test_fitness_rejects_non_sign(cuda_device):
         hga.evaluate(np.ones((2, 4, 4), np.int8), "f3")
 
 
-@pytest.mark.parametrize("m", [36, 40, 44, 48, 52, 56, 60, 64])
+@pytest.mark.parametrize("m", [4, 16, 20, 32, 36, 40, 44, 48, 52, 56, 60, 64])
 def test_fitness_tensor_core_path_matches_popc_path(m, cuda_device, monkeypatch):
-    """Orders 36..64 run on tcgen05 (kind::i8 Gram in TMEM); HGA_FITNESS_TC=0
-    selects the XOR+POPC kernel.  Both must equal the oracle bit for bit,
+    """HGA_FITNESS_TC=all runs the Gram on tcgen05 (kind::i8, TMEM) at every
+    order, HGA_FITNESS_TC=0 on the XOR+POPC kernel (default: tensor cores
+    from m = 48).  Both must equal the oracle bit for bit,
     for odd batch sizes (the last MMA pair half empty) and fixtures."""
     rng = np.random.default_rng(m)
     pops = [oracle.random_balanced(m, 2047, 5 + m, 1, 0, 0),
@@ -94,6 +95,7 @@ def test_fitness_tensor_core_path_matches_popc_path(m, cuda_device, monkeypatch)
             pops.append(np.stack([h, -h, h.T]))
     for pop in pops:
         want = oracle.penalties(pop, threads=4)
+        monkeypatch.setenv("HGA_FITNESS_TC", "all")  # tensor cores at every order
         got_tc = hga.penalties(pop)
         monkeypatch.setenv("HGA_FITNESS_TC", "0")
         got_pc = hga.penalties(pop)
@@ -105,8 +107,9 @@ def test_fitness_tensor_core_path_matches_popc_path(m, cuda_device, monkeypatch)
             assert np.array_equal(hga.evaluate(pop, key), want[:, ("f1", "f2").index(key)])
 
 
-@pytest.mark.parametrize("m", [36, 48, 60, 64])
-def test_fitness_tensor_core_rejects_non_sign(m, cuda_device):
+@pytest.mark.parametrize("m", [20, 36, 48, 60, 64])
+def test_fitness_tensor_core_rejects_non_sign(m, cuda_device, monkeypatch):
+    monkeypatch.setenv("HGA_FITNESS_TC", "all")
     base = oracle.random_balanced(m, 5, 3, 1, 0, 0)
     for (k, r, c, v) in ((0, 0, 0, 0), (4, m - 1, m - 1, 2), (2, m // 2, m - 1, -3), (3, 7, 17, 0)):
         pop = base.copy()
