@@ -681,6 +681,195 @@ __device__ __forceinline__ void group_tiles(const TileCtx& C, int64_t first, int
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------- throughput tiles
+// Large populations (many tiles per group) at orders 28..40: one thread per
+// child.  Every warp runs the whole straight-line pair chain of its own 32
+// children, so all warps of the SM execute the same instruction stream (the
+// team-of-4 split makes four warps run four different 10-20 KB code regions,
+// which misses the instruction cache at these orders); a tile is 64 pairs =
+// 128 children = the 128 threads of a group.  Same survivors, crossover
+// points, plans and operator order as the team tiles: identical populations.
+constexpr int kTPPairs = 64;
+constexpr int kTPOff = 2 * kTPPairs;
+constexpr int kTPPlanStride = 68;  // nc + 2 nr <= 64 (else the team tiles are used)
+
+struct TileSharedTP {
+    int16_t point[kTPPairs];
+    int32_t pidx[kTPOff];
+};
+
+template <int M>
+__device__ __forceinline__ void tp_prepare(const TileCtx& C, TileSharedTP& S, int64_t p0, int cnt, LocalAcc& L) {
+    const int t = threadIdx.x & (kR2Threads - 1);
+    const int64_t N = C.N;
+    const bool act = t < 2 * cnt;
+    const int64_t slot = (int64_t)(t & 1) * N + p0 + (t >> 1);
+    int64_t f = 0;
+    if (act) {
+        const unsigned long long kv = survivor_by_rank(*C.V, feistel2_inv((uint32_t)slot, *C.fkey));
+        S.pidx[t] = (int32_t)(kv & 0xffffffffu);
+        f = (int64_t)(kv >> 32);
+        C.f_new[slot] = f;
+        const unsigned long long key = ((unsigned long long)f << 32) | (unsigned long long)slot;
+        L.best = min(L.best, key);
+        L.pbest = min(L.pbest, key);
+    }
+    local_hist_add(L, C.ws, C.hslot, act, (uint32_t)(f >> C.gshift));
+    if (t < cnt) {
+        const int64_t p = p0 + t;
+        const U4 r = draw4(C.A->seed, (uint32_t)p, (uint32_t)(p >> 32), C.gen, (uint32_t)kPCrossover);
+        S.point[t] = (int16_t)(1 + bounded(r.x, (uint32_t)(M - 1)));
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void tp_gather(const TileCtx& C, const TileSharedTP& S, uint4* rows, int cnt) {
+    using G = RunGeom<M>;
+    const int t = threadIdx.x & (kR2Threads - 1);
+    for (int x = t; x < 2 * cnt * G::U; x += kR2Threads) {
+        const int pi = x / G::U, u = x - (x / G::U) * G::U;
+        cp_async16(rows + pi * G::STU + u, reinterpret_cast<const uint4*>(C.pop_old + (int64_t)S.pidx[pi] * G::MW) + u);
+    }
+}
+
+template <int M, int VM>
+__device__ __forceinline__ void tp_compute(const TileCtx& C, const TileSharedTP& S, int8_t* plan, uint4* rows,
+                                           int64_t p0, int cnt, LocalAcc& L) {
+    using G = RunGeom<M>;
+    constexpr int W = G::W;
+    const int64_t N = C.N;
+    const int t = threadIdx.x & (kR2Threads - 1);
+    const int noff = 2 * cnt;
+    const int nc = C.nc, nr = C.nr;
+    const int g = C.g;
+    // b'. parents to the new population's parent slots (block A, then block B)
+    for (int x = t; x < noff * G::U; x += kR2Threads) {
+        const int b = x / (cnt * G::U);
+        const int r = x - b * cnt * G::U;
+        const int q = r / G::U, u = r - q * G::U;
+        reinterpret_cast<uint4*>(C.pop_new + ((int64_t)b * N + p0 + q) * G::MW)[u] = rows[(2 * q + b) * G::STU + u];
+    }
+    group_sync(g);
+    // c. column-block crossover in place
+    for (int x = t; x < cnt * M; x += kR2Threads) {
+        const int q = x / M, j = x - q * M;
+        if (j >= S.point[q]) {
+            uint32_t* ra = reinterpret_cast<uint32_t*>(rows + (2 * q) * G::STU) + j * W;
+            uint32_t* rb = reinterpret_cast<uint32_t*>(rows + (2 * q + 1) * G::STU) + j * W;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const uint32_t tmp = ra[w];
+                ra[w] = rb[w];
+                rb[w] = tmp;
+            }
+        }
+    }
+    group_sync(g);
+    // d. this thread's child: its Philox plan, then the mutation in plan order
+    //    (engine.py:361-373: columns outer, row pairs inner), then e. its pair chain
+    const bool active = t < noff;
+    int64_t value = 0;
+    const int64_t slot = 2 * N + (int64_t)(t & 1) * N + p0 + (t >> 1);
+    if (active) {
+        const int per_off = nc + 2 * nr;
+        const int q = t >> 1;
+        int64_t prow = (t & 1) ? N + p0 + q : p0 + q;  // plan row as engine.py: O1 -> p, O2 -> N + p
+        if (C.A->strategy == HGA_MUT_SHARED) prow = 0;
+        int8_t* pl = plan + t * kTPPlanStride;
+        for (int blk = 0; blk * 4 < per_off; ++blk) {
+            const U4 r = draw4(C.A->seed, (uint32_t)prow, (uint32_t)blk | ((uint32_t)(prow >> 32) << 16), C.gen,
+                               (uint32_t)kPMutCol);
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) {
+                const int e = blk * 4 + e4;
+                if (e < per_off)
+                    pl[e] = (int8_t)(e < nc ? 1 + bounded(pick(r, e4), (uint32_t)(M - 1)) : bounded(pick(r, e4), (uint32_t)M));
+            }
+        }
+        uint32_t* row = reinterpret_cast<uint32_t*>(rows + t * G::STU);
+        for (int jc = 0; jc < nc; ++jc) {
+            uint32_t* cw = row + pl[jc] * W;
+            uint32_t w0 = cw[0], w1 = W > 1 ? cw[W > 1 ? 1 : 0] : 0u;
+            for (int ir = 0; ir < nr; ++ir) {
+                const int ra = pl[nc + ir], rb = pl[nc + nr + ir];
+                const uint32_t va = (W > 1 && (ra >> 5)) ? w1 : w0, vb = (W > 1 && (rb >> 5)) ? w1 : w0;
+                const uint32_t flip = ((va >> (ra & 31)) ^ (vb >> (rb & 31))) & 1u;  // rows differ: swap
+                const uint32_t ma = flip << (ra & 31), mb = flip << (rb & 31);
+                if (W > 1 && (ra >> 5)) w1 ^= ma;
+                else w0 ^= ma;
+                if (W > 1 && (rb >> 5)) w1 ^= mb;
+                else w0 ^= mb;
+            }
+            cw[0] = w0;
+            if constexpr (W > 1) cw[1] = w1;
+        }
+        uint32_t c[G::MW];
+#pragma unroll
+        for (int u = 0; u < G::U; ++u) {
+            const uint4 v = rows[t * G::STU + u];
+            c[4 * u] = v.x;
+            c[4 * u + 1] = v.y;
+            c[4 * u + 2] = v.z;
+            c[4 * u + 3] = v.w;
+        }
+        Sums s{0, 0, 0, 0};
+        pair_sums<M, VM, 1>(c, s);
+        value = variant_value<M, VM>(s, G::NP);
+        C.f_new[slot] = value;
+        L.best = min(L.best, ((unsigned long long)value << 32) | (unsigned long long)slot);
+    }
+    local_hist_add(L, C.ws, C.hslot, active, (uint32_t)(value >> C.gshift));
+    group_sync(g);
+    // g. coalesced store of the children (O1 block, then O2 block)
+    for (int x = t; x < noff * G::U; x += kR2Threads) {
+        const int b = x / (cnt * G::U);
+        const int r = x - b * cnt * G::U;
+        const int q = r / G::U, u = r - q * G::U;
+        reinterpret_cast<uint4*>(C.pop_new + (2 * N + (int64_t)b * N + p0 + q) * G::MW)[u] = rows[(2 * q + b) * G::STU + u];
+    }
+    group_sync(g);
+}
+
+template <int M, int VM>
+__device__ __forceinline__ void group_tiles_tp(const TileCtx& C, int64_t first, int64_t stride, int64_t ntiles,
+                                               uint4* rows0, uint4* rows1, TileSharedTP* S0, TileSharedTP* S1,
+                                               int8_t* plan, LocalAcc& L) {
+    if (first >= ntiles) return;
+    const int64_t N = C.N;
+    uint4* rows[2] = {rows0, rows1};
+    TileSharedTP* S[2] = {S0, S1};
+    auto cnt_of = [&](int64_t tile) { return (int)min((int64_t)kTPPairs, N - tile * kTPPairs); };
+    tp_prepare<M>(C, *S[0], first * kTPPairs, cnt_of(first), L);
+    group_sync(C.g);
+    tp_gather<M>(C, *S[0], rows[0], cnt_of(first));
+    cp_async_commit();
+    int cur = 0;
+    for (int64_t tile = first; tile < ntiles; tile += stride) {
+        const int64_t nxt = tile + stride;
+        if (nxt < ntiles) tp_prepare<M>(C, *S[cur ^ 1], nxt * kTPPairs, cnt_of(nxt), L);
+        group_sync(C.g);
+        if (nxt < ntiles) tp_gather<M>(C, *S[cur ^ 1], rows[cur ^ 1], cnt_of(nxt));
+        cp_async_commit();
+        cp_async_wait<1>();
+        group_sync(C.g);
+        tp_compute<M, VM>(C, *S[cur], plan, rows[cur], tile * kTPPairs, cnt_of(tile), L);
+        cur ^= 1;
+    }
+    cp_async_wait<0>();
+}
+
+// dynamic shared memory of one tile group
+template <int M, bool TP>
+__host__ __device__ constexpr size_t run_rows_bytes() {
+    return (size_t)(TP ? kTPOff : kTileOff) * RunGeom<M>::STU * 16;
+}
+template <int M, bool TP>
+__host__ __device__ constexpr size_t run_group_bytes() {
+    return TP ? 2 * run_rows_bytes<M, TP>() + 2 * ((sizeof(TileSharedTP) + 15) & ~(size_t)15) +
+                    (size_t)kTPOff * kTPPlanStride
+              : 2 * run_rows_bytes<M, TP>() + 2 * ((sizeof(TileShared) + 15) & ~(size_t)15);
+}
+
 constexpr int kMaxNb = 512;  // prefix scan: one pass of <= 16 warps
 
 // Block-wide exclusive prefix of packed per-range counts (lt | eq << 16) into
@@ -730,7 +919,7 @@ __device__ inline void scan_ranges(const uint32_t* cnt, int n, uint32_t* lt_pre,
 // same ranks, so they produce identical runs.  Measured: ONE is slower at
 // order 20 (22.8 vs 17.2 us/generation: reading all keys and the 8-lane
 // lookups cost more than the second barrier saves), so it is opt-in.
-template <int M, int VM, int GROUPS, bool ONE>
+template <int M, int VM, int GROUPS, bool ONE, bool TP>
 __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t sscr[32];
@@ -759,18 +948,22 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     const int nc = A.strategy == HGA_MUT_MULTI ? A.nc : 1;
     const int nr = A.strategy == HGA_MUT_MULTI ? A.nr : 1;
     const int gshift = P.gshift;
-    const int64_t ntiles = (N + kR2Pairs - 1) / kR2Pairs;
+    const int64_t ntiles = TP ? (N + kTPPairs - 1) / kTPPairs : (N + kR2Pairs - 1) / kR2Pairs;
     // warps taking part in the select scans (the rest only meet the barriers)
     const int pw_sel = (int)min((int64_t)nw, (chunk / kSelItems + 31) / 32);
     const int pw_pre = (nb + 31) / 32;  // nb <= kMaxNb = 32 * 32
     // dynamic shared memory: per group, two row buffers and two tile records
-    constexpr size_t kRowsBytes = (size_t)kTileOff * G::STU * 16;
-    constexpr size_t kGroupBytes = 2 * kRowsBytes + 2 * ((sizeof(TileShared) + 15) & ~(size_t)15);
+    constexpr size_t kRowsBytes = run_rows_bytes<M, TP>();
+    constexpr size_t kGroupBytes = run_group_bytes<M, TP>();
     unsigned char* gbase = smem + (size_t)g * kGroupBytes;
     uint4* rows0 = reinterpret_cast<uint4*>(gbase);
     uint4* rows1 = reinterpret_cast<uint4*>(gbase + kRowsBytes);
     TileShared* S0 = reinterpret_cast<TileShared*>(gbase + 2 * kRowsBytes);
     TileShared* S1 = reinterpret_cast<TileShared*>(gbase + 2 * kRowsBytes + ((sizeof(TileShared) + 15) & ~(size_t)15));
+    constexpr size_t kTPS = (sizeof(TileSharedTP) + 15) & ~(size_t)15;
+    TileSharedTP* T0 = reinterpret_cast<TileSharedTP*>(gbase + 2 * kRowsBytes);
+    TileSharedTP* T1 = reinterpret_cast<TileSharedTP*>(gbase + 2 * kRowsBytes + kTPS);
+    int8_t* tplan = reinterpret_cast<int8_t*>(gbase + 2 * kRowsBytes + 2 * kTPS);
 
     int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
     int parity = (int)A.state[3];
@@ -993,7 +1186,12 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
             TileCtx C{&A, ws, &V, &fkey, pop_old, pop_new, f_new, N, nc, nr, (uint64_t)gen, gp, gshift, g,
                       (timing_blk && g == 0 && gi < 64) ? ws->tstamp[gi] : nullptr,
                       ONE ? keys_base + (int64_t)(parity ^ 1) * kstride : nullptr, hslot};
-            group_tiles<M, VM, ONE>(C, (int64_t)bid * GROUPS + g, (int64_t)nb * GROUPS, ntiles, rows0, rows1, S0, S1, L);
+            if constexpr (TP)
+                group_tiles_tp<M, VM>(C, (int64_t)bid * GROUPS + g, (int64_t)nb * GROUPS, ntiles, rows0, rows1, T0, T1,
+                                      tplan, L);
+            else
+                group_tiles<M, VM, ONE>(C, (int64_t)bid * GROUPS + g, (int64_t)nb * GROUPS, ntiles, rows0, rows1, S0, S1,
+                                        L);
         }
         if (timing && gi < 64) ws->tstamp[gi][8] = gtimer();
         // flush the CTA's histogram window, key range and best keys
@@ -1151,6 +1349,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
 
 int run2_granule_shift(uint32_t fit_var);
 bool run2_supported(const hga_run_args* a);
+constexpr uint32_t kRunForceTP = 1u << 16;  // internal (tests): throughput tiles whatever the size
 inline bool run2_use_onebar(const hga_run_args* a) {
     return run2_onebar(a->n_pairs) && (a->flags & HGA_RUN_ONE_BARRIER) != 0;
 }
@@ -1168,14 +1367,14 @@ constexpr int run_groups() {
     return M <= 24 ? 5 : (M <= 36 ? 4 : 2);
 }
 
-template <int M, int VM, bool ONE>
+template <int M, int VM, bool ONE, bool TP = false>
 int launch_run_v2_k(const hga_run_args* a, cudaStream_t st) {
-    constexpr int GROUPS = run_groups<M>();
+    constexpr int GROUPS = TP ? 2 : run_groups<M>();
     Run2Params P;
     P.a = *a;
     P.gshift = run2_granule_shift(a->fit_var);
-    const int smem = GROUPS * (2 * kTileOff * RunGeom<M>::STU * 16 + 2 * (int)((sizeof(TileShared) + 15) & ~(size_t)15));
-    auto kern = k_run_v3<M, VM, GROUPS, ONE>;
+    const int smem = GROUPS * (int)run_group_bytes<M, TP>();
+    auto kern = k_run_v3<M, VM, GROUPS, ONE, TP>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1197,6 +1396,13 @@ int launch_run_v2_k(const hga_run_args* a, cudaStream_t st) {
 template <int M, int VM>
 int launch_run_v2_mv(const hga_run_args* a, cudaStream_t st) {
     if (run2_use_onebar(a)) return launch_run_v2_k<M, VM, true>(a, st);
+    if constexpr (M >= 28 && M <= 40) {
+        // throughput tiles once every group gets several of them (or when forced, for tests)
+        const int nc = a->strategy == HGA_MUT_MULTI ? a->nc : 1, nr = a->strategy == HGA_MUT_MULTI ? a->nr : 1;
+        const bool fits = nc + 2 * nr <= kTPPlanStride - 4;
+        const bool many = a->n_pairs >= (int64_t)kTPPairs * 2 * sm_count_cached() * 4;
+        if (fits && (many || (a->flags & kRunForceTP))) return launch_run_v2_k<M, VM, false, true>(a, st);
+    }
     return launch_run_v2_k<M, VM, false>(a, st);
 }
 
