@@ -682,8 +682,7 @@ __device__ __forceinline__ void group_tiles(const TileCtx& C, int64_t first, int
 }
 
 // ---------------------------------------------------------------- throughput tiles
-// Large populations (many tiles per group) at orders 28..40: one thread per
-// child.  Every warp runs the whole straight-line pair chain of its own 32
+// Orders 24..40 (the default there): one thread per child.  Every warp runs the whole straight-line pair chain of its own 32
 // children, so all warps of the SM execute the same instruction stream (the
 // team-of-4 split makes four warps run four different 10-20 KB code regions,
 // which misses the instruction cache at these orders); a tile is 64 pairs =
@@ -1349,7 +1348,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
 
 int run2_granule_shift(uint32_t fit_var);
 bool run2_supported(const hga_run_args* a);
-constexpr uint32_t kRunForceTP = 1u << 16;  // internal (tests): throughput tiles whatever the size
+constexpr uint32_t kRunTeamTiles = 1u << 16;  // internal (tests, timing): team-of-four tiles instead of throughput tiles
 inline bool run2_use_onebar(const hga_run_args* a) {
     return run2_onebar(a->n_pairs) && (a->flags & HGA_RUN_ONE_BARRIER) != 0;
 }
@@ -1367,9 +1366,16 @@ constexpr int run_groups() {
     return M <= 24 ? 5 : (M <= 36 ? 4 : 2);
 }
 
+template <int M>
+constexpr int run_groups_tp() {
+    // one thread per child holds the whole chain's live values: ~125 registers
+    // at m = 24 (four groups fit), ~250 at m = 28..40 (two groups)
+    return M <= 24 ? 4 : 2;
+}
+
 template <int M, int VM, bool ONE, bool TP = false>
 int launch_run_v2_k(const hga_run_args* a, cudaStream_t st) {
-    constexpr int GROUPS = TP ? 2 : run_groups<M>();
+    constexpr int GROUPS = TP ? run_groups_tp<M>() : run_groups<M>();
     Run2Params P;
     P.a = *a;
     P.gshift = run2_granule_shift(a->fit_var);
@@ -1396,12 +1402,15 @@ int launch_run_v2_k(const hga_run_args* a, cudaStream_t st) {
 template <int M, int VM>
 int launch_run_v2_mv(const hga_run_args* a, cudaStream_t st) {
     if (run2_use_onebar(a)) return launch_run_v2_k<M, VM, true>(a, st);
-    if constexpr (M >= 28 && M <= 40) {
-        // throughput tiles once every group gets several of them (or when forced, for tests)
+    if constexpr (M >= 24 && M <= 40) {
+        // throughput tiles unless the plan does not fit their per-child slot
+        // (kRunTeamTiles forces the team tiles: A/B timing, tests).  Measured
+        // (scripts/tp_threshold.py): faster from m = 24 on (m = 28, 4N = 125,000:
+        // 35.7 -> 27.7 us/generation; m = 36, 4N = 1.25M: 481 -> 425), slower
+        // at m = 20 (17.0 -> 18.6), where the team tiles stay.
         const int nc = a->strategy == HGA_MUT_MULTI ? a->nc : 1, nr = a->strategy == HGA_MUT_MULTI ? a->nr : 1;
         const bool fits = nc + 2 * nr <= kTPPlanStride - 4;
-        const bool many = a->n_pairs >= (int64_t)kTPPairs * 2 * sm_count_cached() * 4;
-        if (fits && (many || (a->flags & kRunForceTP))) return launch_run_v2_k<M, VM, false, true>(a, st);
+        if (fits && !(a->flags & kRunTeamTiles)) return launch_run_v2_k<M, VM, false, true>(a, st);
     }
     return launch_run_v2_k<M, VM, false>(a, st);
 }

@@ -449,15 +449,16 @@ def test_one_barrier_loop_matches_two_barrier(m, N, fit, nc, nr, sw, cuda_device
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
 
 
-@pytest.mark.parametrize("m,N,fit,nc,nr,mut,sw", [(28, 1000, "f2", 2, 3, "multi", None), (36, 600, "f1", 3, 3, "multi", None),
+@pytest.mark.parametrize("m,N,fit,nc,nr,mut,sw", [(24, 333, "sq", 2, 5, "multi", 4), (24, 20000, "f2", 1, 10, "multi", None),
+                                                   (28, 1000, "f2", 2, 3, "multi", None), (36, 600, "f1", 3, 3, "multi", None),
                                                    (40, 300, "f2", 1, 12, "multi", 5), (32, 257, "f2", 1, 2, "shared", None),
                                                    (36, 129, "f1", 1, 1, "per-matrix", None), (28, 70, "sq", 5, 2, "multi", 3)])
 def test_throughput_tiles_match_team_tiles(m, N, fit, nc, nr, mut, sw, cuda_device, monkeypatch):
-    """Large populations at orders 28..40 use one thread per child (the whole
-    pair chain per warp); forced here at small N, it must give the same runs
-    as the team-of-four tiles (same survivors, points, plans, operator order)."""
+    """Orders 24..40 use one thread per child (the whole pair chain per warp)
+    by default; it must give the same runs as the team-of-four tiles (same
+    survivors, points, plans, operator order)."""
     out = []
-    for flags in (0, 1 << 16):  # internal kRunForceTP
+    for flags in (0, 1 << 16):  # internal kRunTeamTiles
         monkeypatch.setattr(engine, "_RUN_FLAGS", flags)
         cfg = engine.GAConfig(order=m, population=N, seed=13, fitness=fit, mutation_cols=nc, mutation_row_pairs=nr,
                               mutation=mut, stall_window=sw, max_iterations=500)
