@@ -30,6 +30,7 @@
 // does 2 * 64 * N * 64 MACs (N = 16 ceil(m/16)) and the epilogue ~2 * 64 * N
 // integer ops, both far below the HBM time at these orders.
 #include <cstdint>
+#include <cstdlib>
 
 #include "hga_common.cuh"
 
@@ -133,10 +134,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         : "r"(taddr));
 }
 
-template <int M, int VM>
+template <int M, int VM, bool OW>
 __global__ void __launch_bounds__(kThreads, 1)
     k_fit_i8_tc(const int8_t* __restrict__ pop, int64_t n, uint32_t vm_out, int64_t* __restrict__ f1,
-                int64_t* __restrict__ f2, int64_t* __restrict__ orth, int64_t* __restrict__ sq, int32_t* bad_flag) {
+                int64_t* __restrict__ f2, int64_t* __restrict__ orth, int64_t* __restrict__ sq, int32_t* bad_flag,
+                int rowmajor) {
     using G = Geo<M>;
     constexpr int UT = 2 * kB;  // tiles per pipeline unit
     extern __shared__ __align__(1024) uint8_t smem[];  // G::STAGES x UT x G::TILE
@@ -183,9 +185,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < G::PER; ++i) {
             const int g = (i * 2 + half) * 32 + lane;  // piece of the tile's P consecutive matrices
-            const int src = g * G::GR;
-            const int e = src / (M * M), o = src - e * (M * M);
-            const int r = o / M, c = o - (o / M) * M;
+            int e, r, c;
+            if (rowmajor) {  // legacy order (A/B switch): pieces in source order
+                const int src = g * G::GR;
+                e = src / (M * M);
+                const int o = src - e * (M * M);
+                r = o / M;
+                c = o - r * M;
+            } else {
+                // Bank-conflict-free order: within each block of 8 rows, column group
+                // by column group, row by row, then the 16-byte row segment's pieces.
+                // The lanes of one shared-memory phase (8 x 16 B, 16 x 8 B or 32 x 4 B)
+                // then write / read the 128 contiguous bytes of one core-matrix column
+                // (8 rows x 16 B) instead of the same 16 bytes of 4 column groups
+                // (4-way conflicts); a warp still covers whole 8-row blocks of the
+                // source, so global accesses stay coalesced.
+                constexpr int SUB = 16 / G::GR, RB = 8 * (M / G::GR);  // pieces per full 16-B segment / row block
+                e = g / G::NG;
+                const int o = g - e * G::NG;
+                const int rb = o / RB, o2 = o - rb * RB;
+                const int rows = min(8, M - 8 * rb);
+                const int cg = o2 / (rows * SUB), o3 = o2 - cg * (rows * SUB);
+                const int subs = min(16, M - 16 * cg) / G::GR;
+                const int rl = o3 / subs;
+                r = 8 * rb + rl;
+                c = 16 * cg + (o3 - rl * subs) * G::GR;
+            }
+            const int src = e * (M * M) + r * M + c;
             const int dst = e * G::NCG * G::SBO + (c >> 4) * G::SBO + (r >> 3) * 128 + (r & 7) * 16 + (c & 15);
             tab[i] = g < G::P * G::NG ? ((uint32_t)src | ((uint32_t)dst << 16)) : 0xFFFFFFFFu;
         }
@@ -283,11 +309,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         // warps to interleave (one warp alone is latency-bound on the reductions).
         const int q = warp & 3, grp = warp >> 2;  // TMEM lane quarter, epilogue group
         const int jj = lane >> 4;
-        // Gram symmetry: quarter q holds rows 16 lq .. 16 lq + 15 of its matrix
-        // (lq = local quarter); it reads only column blocks cb >= lq and counts
-        // the off-diagonal blocks twice.
+        // Gram symmetry: each unordered pair of 16-row/16-column blocks {i, j} is
+        // read once, off-diagonal blocks counted twice.  Quarter q holds row
+        // block lq of its matrix and may read any column block of it (block
+        // (q, j) is the transpose of (j, q)).  Packed tiles (P > 1) read the
+        // upper triangle, cb >= lq.  One matrix per tile (m = 36..64,
+        // NCG = 3 or 4): quarter q reads the cyclic blocks q, q+1, .. q+NCG/2
+        // (mod NCG; the d = NCG/2 block of an even NCG only for q < NCG/2), so
+        // the quarters read 2/2/2/0 (NCG = 3) or 3/3/2/2 (NCG = 4) blocks per
+        // matrix instead of 3/2/1/0 or 4/3/2/1 -- the slowest warp of the group
+        // sets the pace.
         const int lq = G::P > 1 ? q % G::NCG : q;
         const int cs = G::P > 1 ? G::COLS * (q / G::NCG) : 0;  // this quarter's matrix block
+        constexpr int NB = G::P > 1 ? G::NCG : G::NCG / 2 + 1;  // block slots per pair
+        // (column block, weight) of slot d for this quarter; weight 0 = skip
+        int bcol[NB];
+        uint32_t bw[NB];
+#pragma unroll
+        for (int d = 0; d < NB; ++d) {
+            if constexpr (G::P > 1) {
+                bcol[d] = d;
+                bw[d] = d < lq ? 0u : (d == lq ? 1u : 2u);
+            } else {
+                bcol[d] = (q + d) % G::NCG;
+                const bool on = q < G::NCG && (d < G::NCG / 2 || (G::NCG & 1) || q < G::NCG / 2);
+                bw[d] = on ? (d == 0 ? 1u : 2u) : 0u;
+            }
+        }
+        // one tcgen05.wait::ld per unit when both pairs' blocks fit in registers
+        constexpr bool kOneWait = OW && G::P == 1 && kB * NB <= 4;
         for (int it = grp;; it += kEpiGroups) {
             const int64_t u = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
             if (u >= nunits) break;
@@ -295,24 +345,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull[a], (it / kSlots) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             uint32_t(&pp)[kB][2][4][3] = part[grp][(it / kEpiGroups) & 1];
+            uint32_t vall[kOneWait ? kB : 1][NB][16];
+            if constexpr (kOneWait) {
+#pragma unroll
+                for (int b = 0; b < kB; ++b) {
+                    const uint32_t taddr = tbase + (uint32_t)(a * kSlotCols + b * 64) + ((uint32_t)(32 * q) << 16);
+#pragma unroll
+                    for (int d = 0; d < NB; ++d)
+                        if (bw[d]) tmem_ld16(taddr + (uint32_t)(16 * bcol[d]), vall[b][d]);
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            }
 #pragma unroll
             for (int b = 0; b < kB; ++b) {
-                uint32_t v[G::NCG][16];
-                const uint32_t taddr = tbase + (uint32_t)(a * kSlotCols + b * 64 + cs) + ((uint32_t)(32 * q) << 16);
+                uint32_t(&v)[NB][16] = vall[kOneWait ? b : 0];
+                if constexpr (!kOneWait) {
+                    const uint32_t taddr = tbase + (uint32_t)(a * kSlotCols + b * 64 + cs) + ((uint32_t)(32 * q) << 16);
 #pragma unroll
-                for (int cb = 0; cb < G::NCG; ++cb)
-                    if (cb >= lq) tmem_ld16(taddr + (uint32_t)(16 * cb), v[cb]);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                // weighted row sums over the upper-triangle blocks (padded entries are 0)
+                    for (int d = 0; d < NB; ++d)
+                        if (bw[d]) tmem_ld16(taddr + (uint32_t)(16 * bcol[d]), v[d]);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
+                // weighted row sums over the chosen blocks (padded entries are 0)
                 uint32_t pa[4] = {0, 0, 0, 0}, pn[4] = {0, 0, 0, 0}, ps[4] = {0, 0, 0, 0};  // 4 chains for ILP
 #pragma unroll
-                for (int cb = 0; cb < G::NCG; ++cb) {
-                    if (cb < lq) continue;
-                    const uint32_t wgt = cb == lq ? 1u : 2u;
+                for (int d = 0; d < NB; ++d) {
+                    if (!bw[d]) continue;
+                    const uint32_t wgt = bw[d];
                     uint32_t ba[4] = {0, 0, 0, 0}, bn[4] = {0, 0, 0, 0}, bs[4] = {0, 0, 0, 0};
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
-                        const int g = (int)v[cb][e];
+                        const int g = (int)v[d][e];
                         if constexpr ((VM & HGA_VAR_F1) != 0) ba[e & 3] += (uint32_t)abs(g);
                         if constexpr ((VM & (HGA_VAR_F2 | HGA_VAR_ORTH)) != 0) bn[e & 3] += (g != 0);
                         if constexpr ((VM & HGA_VAR_SQ) != 0) bs[e & 3] += (uint32_t)(g * g);
@@ -373,10 +436,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512) : "memory");
 }
 
-template <int M, int VM>
+template <int M, int VM, bool OW>
 static int launch_tc(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth, int64_t* sq,
                      int32_t* bad, cudaStream_t st) {
-    auto kern = k_fit_i8_tc<M, VM>;
+    auto kern = k_fit_i8_tc<M, VM, OW>;
     constexpr int smem = Geo<M>::STAGES * 2 * kB * Geo<M>::TILE;
     static bool attr = false;
     if (!attr) {
@@ -386,17 +449,28 @@ static int launch_tc(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int6
     }
     const int64_t nunits = (n + kB * Geo<M>::MPP - 1) / (kB * Geo<M>::MPP);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nunits, sm_count_cached()));
-    kern<<<grid, kThreads, smem, st>>>(pop, n, v, f1, f2, orth, sq, bad);
+    static const int rowmajor = std::getenv("HGA_TC_ROWMAJOR") != nullptr;  // A/B: legacy piece order
+    kern<<<grid, kThreads, smem, st>>>(pop, n, v, f1, f2, orth, sq, bad, rowmajor);
     return to_rc(cudaGetLastError());
 }
 
 template <int M>
 static int launch_tc_m(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth,
                        int64_t* sq, int32_t* bad, cudaStream_t st) {
+    // HGA_TC_ONEWAIT: one tcgen05.wait::ld per unit at NCG = 3 (A/B switch)
+    static const bool ow = std::getenv("HGA_TC_ONEWAIT") != nullptr;
+    if constexpr (Geo<M>::P == 1 && Geo<M>::NCG == 3) {
+        if (ow) {
+            if ((v & ~(HGA_VAR_F2 | HGA_VAR_ORTH)) == 0)
+                return launch_tc<M, HGA_VAR_F2 | HGA_VAR_ORTH, true>(pop, n, v, f1, f2, orth, sq, bad, st);
+            if (v == HGA_VAR_F1) return launch_tc<M, HGA_VAR_F1, true>(pop, n, v, f1, f2, orth, sq, bad, st);
+            return launch_tc<M, HGA_VAR_ALL, true>(pop, n, v, f1, f2, orth, sq, bad, st);
+        }
+    }
     if ((v & ~(HGA_VAR_F2 | HGA_VAR_ORTH)) == 0)
-        return launch_tc<M, HGA_VAR_F2 | HGA_VAR_ORTH>(pop, n, v, f1, f2, orth, sq, bad, st);
-    if (v == HGA_VAR_F1) return launch_tc<M, HGA_VAR_F1>(pop, n, v, f1, f2, orth, sq, bad, st);
-    return launch_tc<M, HGA_VAR_ALL>(pop, n, v, f1, f2, orth, sq, bad, st);
+        return launch_tc<M, HGA_VAR_F2 | HGA_VAR_ORTH, false>(pop, n, v, f1, f2, orth, sq, bad, st);
+    if (v == HGA_VAR_F1) return launch_tc<M, HGA_VAR_F1, false>(pop, n, v, f1, f2, orth, sq, bad, st);
+    return launch_tc<M, HGA_VAR_ALL, false>(pop, n, v, f1, f2, orth, sq, bad, st);
 }
 
 }  // namespace tc

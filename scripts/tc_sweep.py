@@ -1,0 +1,51 @@
+"""int8 fitness sweep at orders 36..64 on one path (for A/B of the fitness kernels).
+
+Usage: python scripts/tc_sweep.py TAG [PATH]   PATH = tc (HGA_FITNESS_TC=all) | popc (HGA_FITNESS_TC=0) | default
+One JSON line per (m, variant): best of 10 CUDA-event timings after 3 warm-ups.
+"""
+import json
+import os
+import sys
+from pathlib import Path
+
+tag = sys.argv[1] if len(sys.argv) > 1 else "run"
+path = sys.argv[2] if len(sys.argv) > 2 else "tc"
+if path != "default":
+    os.environ["HGA_FITNESS_TC"] = "all" if path == "tc" else "0"
+
+import torch  # noqa: E402
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2208_14961_b200 import engine  # noqa: E402
+from paper_2208_14961_b200._lib import lib  # noqa: E402
+
+orders = [int(x) for x in os.environ.get("ORDERS", "36,40,44,48,52,56,60,64").split(",")]
+n = int(os.environ.get("NMAT", "1000000"))
+st = torch.cuda.current_stream().cuda_stream
+for m in orders:
+    pop = engine.init_population_device(engine.GAConfig(order=m, population=n // 4, seed=2024))
+    for var, name in ((2, "f2"), (1, "f1"), (15, "all")):
+        o = [torch.empty(n, dtype=torch.int64, device="cuda") if var & b else None for b in (1, 2, 4, 8)]
+        ptrs = [x.data_ptr() if x is not None else None for x in o]
+
+        def one():
+            rc = lib.hga_fitness_i8(pop.data_ptr(), n, m, var, *ptrs, None, None, 0, st)
+            assert rc == 0, rc
+
+        for _ in range(3):
+            one()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e30
+        for _ in range(10):
+            s.record()
+            one()
+            e.record()
+            e.synchronize()
+            best = min(best, s.elapsed_time(e) / 1e3)
+        byts = n * (m * m + 8 * bin(var).count("1"))
+        print(json.dumps({"tag": tag, "path": path, "m": m, "n": n, "variant": name, "evals_per_s": n / best,
+                          "GBps": byts / best / 1e9, "frac_hbm": byts / best / 6532.5e9, "us": best * 1e6}),
+              flush=True)
+    del pop
+    torch.cuda.empty_cache()
