@@ -23,8 +23,10 @@
 //     shared-memory stages keep loads, MMAs and epilogues overlapped.
 //   * Epilogue: tcgen05.ld 32x32b.x16 -> registers; each lane sums |g|,
 //     [g != 0] and g^2 over its row; 16-lane shuffles and a 4-warp combine
-//     give the matrix totals.  The same warps check the staged bytes are
-//     +-1 (the v2 kernels' contract: HGA_FLAG_NOT_SIGN otherwise).
+//     give the matrix totals.
+//   * +-1 contract of the v2 kernels (HGA_FLAG_NOT_SIGN otherwise): check
+//     warps scan each staged matrix for bytes outside {0x00, 0x01, 0xFF} and
+//     count the nonzero ones (m^2 iff no entry is 0).
 //
 // Roofline: HBM (m^2 + 8 bytes per matrix).  Per matrix the tensor pipe
 // does 2 * 64 * N * 64 MACs (N = 16 ceil(m/16)) and the epilogue ~2 * 64 * N
@@ -138,8 +140,11 @@ template <int M, int VM, bool OW>
 __global__ void __launch_bounds__(kThreads, 1)
     k_fit_i8_tc(const int8_t* __restrict__ pop, int64_t n, uint32_t vm_out, int64_t* __restrict__ f1,
                 int64_t* __restrict__ f2, int64_t* __restrict__ orth, int64_t* __restrict__ sq, int32_t* bad_flag,
-                int rowmajor) {
+                int flags) {
+    // flags (A/B and bottleneck experiments, HGA_TC_FLAGS; 0 in production): 1 = legacy piece
+    // order; 2 = skip the MMAs, 4 = skip the epilogue reductions, 8 = skip the +-1 check (results invalid)
     using G = Geo<M>;
+    const bool rowmajor = flags & 1;
     constexpr int UT = 2 * kB;  // tiles per pipeline unit
     extern __shared__ __align__(1024) uint8_t smem[];  // G::STAGES x UT x G::TILE
     __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[kSlots], tempty[kSlots];
@@ -215,38 +220,53 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int dst = e * G::NCG * G::SBO + (c >> 4) * G::SBO + (r >> 3) * 128 + (r & 7) * 16 + (c & 15);
             tab[i] = g < G::P * G::NG ? ((uint32_t)src | ((uint32_t)dst << 16)) : 0xFFFFFFFFu;
         }
+        // check warps: this lane's 16-byte chunks (column group, row < m) of one matrix
+        constexpr int kCH = G::NCG * M, kChk = (kCH + 31) / 32;
+        uint32_t coff[kChk];
+#pragma unroll
+        for (int i = 0; i < kChk; ++i) {
+            const int idx = i * 32 + lane, cg = idx / M, r = idx - (idx / M) * M;
+            coff[i] = idx < kCH ? (uint32_t)((cg * G::KP + r) * 16) : 0x80000000u;
+        }
         uint32_t bad = 0;
         int it = 0;
         for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
             const int s = it % G::STAGES;
             if (checker) {
-                // +-1 check of the bytes loader warp lw copied, as soon as they have landed
+                // Check of one staged tile (check warp lw takes tile lw = pair lw / 2,
+                // interleave lw % 2): every byte of each matrix's rows < m and column
+                // groups must be 0x00, 0x01 or 0xFF (entries in {-1, 0, +1}; padding is
+                // 0), and the nonzero bytes (bit 0 set) must number m^2 -- so no entry
+                // is 0.  16-byte chunks of the canonical layout, contiguous per lane
+                // group: conflict-free, independent of the loaders' piece order.
                 mbar_wait(&full[s], (it / G::STAGES) & 1);
+                if (!(flags & 8)) {
+                    const uint8_t* tile = smem + (size_t)(s * UT + lw) * G::TILE;
+                    const int b = lw >> 1;
 #pragma unroll
-                for (int b = 0; b < kB; ++b) {
-                    const int64_t k0 = (int64_t)G::MPP * (kB * u + b) + (int64_t)G::P * j;
-                    const uint32_t lim = k0 < n ? (uint32_t)min((int64_t)G::P, n - k0) * (uint32_t)(M * M) : 0u;
-                    const uint8_t* tile = smem + (size_t)(s * UT + 2 * b + j) * G::TILE;
+                    for (int e = 0; e < G::P; ++e) {
+                        uint32_t cnt = 0;
 #pragma unroll
-                    for (int i = 0; i < G::PER; ++i) {
-                        if (tab[i] == 0xFFFFFFFFu || (tab[i] & 0xFFFFu) >= lim) continue;
-                        const uint8_t* q8 = tile + (tab[i] >> 16);
-                        uint32_t w[G::GR / 4];
-                        if constexpr (G::GR == 16) {
-                            const uint4 x = *reinterpret_cast<const uint4*>(q8);
-                            w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-                        } else if constexpr (G::GR == 8) {
-                            const uint2 x = *reinterpret_cast<const uint2*>(q8);
-                            w[0] = x.x; w[1] = x.y;
-                        } else {
-                            w[0] = *reinterpret_cast<const uint32_t*>(q8);
+                        for (int i = 0; i < kChk; ++i) {
+                            // lanes past the last chunk re-read chunk 0 and mask it to zero (no
+                            // branch: all loads of the matrix can be in flight together)
+                            const uint4 x = *reinterpret_cast<const uint4*>(tile + e * (G::NCG * G::KP * 16) +
+                                                                            (coff[i] & 0xFFFFu));
+                            const uint32_t mk = coff[i] >> 31 ? 0u : 0xFFFFFFFFu;
+                            const uint32_t w4[4] = {x.x & mk, x.y & mk, x.z & mk, x.w & mk};
+#pragma unroll
+                            for (int v4 = 0; v4 < 4; ++v4) {
+                                const uint32_t a8 = w4[v4], h8 = a8 & 0xFEFEFEFEu;
+                                // bits 1..7 equal, and 0xFE excluded (bits 1..7 set => bit 0 set)
+                                bad |= ((h8 ^ (h8 << 1)) & 0xFCFCFCFCu) | ((a8 >> 1) & ~a8 & 0x01010101u);
+                                cnt += a8 & 0x01010101u;  // per-byte counts, <= 4 * 8 < 256
+                            }
                         }
+                        cnt = (cnt * 0x01010101u) >> 24;  // sum of the four byte counts
 #pragma unroll
-                        for (int v4 = 0; v4 < G::GR / 4; ++v4) {
-                            // byte in {0x01, 0xFF}  <=>  a = byte ^ 1 has bit 0 clear and bits 1..7 equal
-                            const uint32_t a8 = w[v4] ^ 0x01010101u, b8 = a8 & 0xFEFEFEFEu;
-                            bad |= (a8 & 0x01010101u) | ((b8 ^ (b8 << 1)) & 0xFCFCFCFCu);
-                        }
+                        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                        const int64_t k = (int64_t)G::MPP * (kB * u + b) + (int64_t)G::P * j + e;
+                        if (k < n && cnt != (uint32_t)(M * M)) bad = 1;
                     }
                 }
                 __syncwarp();
@@ -288,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
 #pragma unroll
-                for (int t = 0; t < UT; ++t) {  // tile t = pair t/2, interleave t%2
+                for (int t = 0; t < ((flags & 2) ? 0 : UT); ++t) {  // tile t = pair t/2, interleave t%2
                     const uint32_t tile = sbase + (uint32_t)((s * UT + t) * G::TILE);
                     const uint32_t d =
                         tbase + (uint32_t)(a * kSlotCols + (t >> 1) * 64) + ((uint32_t)(16 * (t & 1)) << 16);
@@ -344,6 +364,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int a = it % kSlots;
             mbar_wait(&tfull[a], (it / kSlots) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (flags & 4) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[a]);
+                continue;
+            }
             uint32_t(&pp)[kB][2][4][3] = part[grp][(it / kEpiGroups) & 1];
             uint32_t vall[kOneWait ? kB : 1][NB][16];
             if constexpr (kOneWait) {
@@ -373,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (!bw[d]) continue;
                     const uint32_t wgt = bw[d];
                     uint32_t ba[4] = {0, 0, 0, 0}, bn[4] = {0, 0, 0, 0}, bs[4] = {0, 0, 0, 0};
+#pragma unroll
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
                         const int g = (int)v[d][e];
@@ -449,8 +475,11 @@ static int launch_tc(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int6
     }
     const int64_t nunits = (n + kB * Geo<M>::MPP - 1) / (kB * Geo<M>::MPP);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nunits, sm_count_cached()));
-    static const int rowmajor = std::getenv("HGA_TC_ROWMAJOR") != nullptr;  // A/B: legacy piece order
-    kern<<<grid, kThreads, smem, st>>>(pop, n, v, f1, f2, orth, sq, bad, rowmajor);
+    static const int flags = [] {
+        const char* e = std::getenv("HGA_TC_FLAGS");
+        return e ? std::atoi(e) : 0;
+    }();
+    kern<<<grid, kThreads, smem, st>>>(pop, n, v, f1, f2, orth, sq, bad, flags);
     return to_rc(cudaGetLastError());
 }
 

@@ -107,11 +107,14 @@ def test_fitness_tensor_core_path_matches_popc_path(m, cuda_device, monkeypatch)
             assert np.array_equal(hga.evaluate(pop, key), want[:, ("f1", "f2").index(key)])
 
 
-@pytest.mark.parametrize("m", [20, 36, 48, 60, 64])
+@pytest.mark.parametrize("m", list(range(4, 68, 4)))
 def test_fitness_tensor_core_rejects_non_sign(m, cuda_device, monkeypatch):
+    # the tensor-core path checks bytes in {-1, 0, +1} on the staged tiles and
+    # zeros through the Gram diagonal (g_jj = m): cover both halves
     monkeypatch.setenv("HGA_FITNESS_TC", "all")
     base = oracle.random_balanced(m, 5, 3, 1, 0, 0)
-    for (k, r, c, v) in ((0, 0, 0, 0), (4, m - 1, m - 1, 2), (2, m // 2, m - 1, -3), (3, 7, 17, 0)):
+    for (k, r, c, v) in ((0, 0, 0, 0), (4, m - 1, m - 1, 2), (2, m // 2, m - 1, -3), (3, 7 % m, 17 % m, 0),
+                         (1, 1 % m, 1 % m, -2), (0, m - 1, 0, -128), (4, 0, m // 2, 127)):
         pop = base.copy()
         pop[k, r, c] = v
         with pytest.raises(ValueError):
