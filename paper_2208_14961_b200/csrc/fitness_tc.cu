@@ -31,8 +31,11 @@
 // Roofline: HBM (m^2 + 8 bytes per matrix).  Per matrix the tensor pipe
 // does 2 * 64 * N * 64 MACs (N = 16 ceil(m/16)) and the epilogue ~2 * 64 * N
 // integer ops, both far below the HBM time at these orders.
+#include <cuda.h>  // CUtensorMap (types only; the encoder comes from cudaGetDriverEntryPoint)
+
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "hga_common.cuh"
 
@@ -109,6 +112,18 @@ __device__ __forceinline__ void cp_async_piece16(uint32_t dst, const void* src) 
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+// One 16-column group of one matrix (16 B x 64 rows; rows >= m are out of
+// bounds and zero-filled) -> the canonical no-swizzle column group in smem.
+__device__ __forceinline__ void tma_load_cg(uint32_t dst, const CUtensorMap* map, int c0, int64_t k, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(dst), "l"(map), "r"(c0), "r"(0), "r"((int)k), "r"(saddr(bar))
+        : "memory");
+}
+
 // Shared-memory matrix descriptor, no swizzle, MN-major canonical layout.
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
     return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
@@ -140,10 +155,14 @@ template <int M, int VM, bool OW>
 __global__ void __launch_bounds__(kThreads, 1)
     k_fit_i8_tc(const int8_t* __restrict__ pop, int64_t n, uint32_t vm_out, int64_t* __restrict__ f1,
                 int64_t* __restrict__ f2, int64_t* __restrict__ orth, int64_t* __restrict__ sq, int32_t* bad_flag,
-                int flags) {
+                int flags, const __grid_constant__ CUtensorMap tmap) {
     // flags (A/B and bottleneck experiments, HGA_TC_FLAGS; 0 in production): 1 = legacy piece
     // order; 2 = skip the MMAs, 4 = skip the epilogue reductions, 8 = skip the +-1 check (results invalid)
     using G = Geo<M>;
+    // Orders 48 and 64 (row pitch a multiple of 16 B, one matrix per tile): the
+    // stages are filled by TMA, one bulk tensor copy per column group, issued by
+    // one thread; the other orders use cp.async pieces from four loader warps.
+    constexpr bool kTma = G::P == 1 && M % 16 == 0;
     const bool rowmajor = flags & 1;
     constexpr int UT = 2 * kB;  // tiles per pipeline unit
     extern __shared__ __align__(1024) uint8_t smem[];  // G::STAGES x UT x G::TILE
@@ -159,7 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (tid == 0) {
         for (int s = 0; s < G::STAGES; ++s) {
-            mbar_init(&full[s], kLoadWarps * 32);   // one asynchronous cp.async arrival per loader lane
+            // TMA: one expect_tx arrival; cp.async: one asynchronous arrival per loader lane
+            mbar_init(&full[s], kTma ? 1 : kLoadWarps * 32);
             mbar_init(&empty[s], 1 + kCheckWarps);  // MMA commit + the check warps
         }
         for (int a = 0; a < kSlots; ++a) {
@@ -271,6 +291,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
+                continue;
+            }
+            if constexpr (kTma) {
+                if (lw != 0) break;
+                if (lane == 0) {
+                    mbar_wait(&empty[s], ((it / G::STAGES) & 1) ^ 1);
+                    mbar_expect_tx(&full[s], (uint32_t)(UT * G::NCG * G::KP * 16));
+#pragma unroll
+                    for (int t = 0; t < UT; ++t) {  // tile t = pair t / 2, interleave t % 2
+                        // matrices >= n are fully out of bounds: zero-filled, bytes still counted
+                        const int64_t k = (int64_t)G::MPP * (kB * u + (t >> 1)) + (t & 1);
+                        const uint32_t dst = sbase + (uint32_t)((s * UT + t) * G::TILE);
+#pragma unroll
+                        for (int cg = 0; cg < G::NCG; ++cg)
+                            tma_load_cg(dst + (uint32_t)(cg * G::SBO), &tmap, 16 * cg, k, &full[s]);
+                    }
+                }
+                __syncwarp();
                 continue;
             }
             mbar_wait(&empty[s], ((it / G::STAGES) & 1) ^ 1);
@@ -462,6 +500,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512) : "memory");
 }
 
+// 3-D view of the int8 population for TMA: (column, row, matrix), strides m and
+// m^2 bytes; box = 16 columns x kp rows x 1 matrix, out-of-bounds rows zero.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static int encode_pop_map(CUtensorMap* map, const int8_t* pop, int64_t n, int m, int kp) {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    if (!fn) return HGA_E_UNSUPPORTED;
+    const cuuint64_t dims[3] = {(cuuint64_t)m, (cuuint64_t)m, (cuuint64_t)n};
+    const cuuint64_t strides[2] = {(cuuint64_t)m, (cuuint64_t)m * (cuuint64_t)m};
+    const cuuint32_t box[3] = {16u, (cuuint32_t)kp, 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(pop), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : HGA_E_UNSUPPORTED;
+}
+
 template <int M, int VM, bool OW>
 static int launch_tc(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth, int64_t* sq,
                      int32_t* bad, cudaStream_t st) {
@@ -479,7 +542,13 @@ static int launch_tc(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int6
         const char* e = std::getenv("HGA_TC_FLAGS");
         return e ? std::atoi(e) : 0;
     }();
-    kern<<<grid, kThreads, smem, st>>>(pop, n, v, f1, f2, orth, sq, bad, flags);
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    if constexpr (Geo<M>::P == 1 && M % 16 == 0) {
+        int rc = encode_pop_map(&map, pop, n, M, Geo<M>::KP);
+        if (rc != 0) return rc;
+    }
+    kern<<<grid, kThreads, smem, st>>>(pop, n, v, f1, f2, orth, sq, bad, flags, map);
     return to_rc(cudaGetLastError());
 }
 
