@@ -574,9 +574,9 @@ static int launch_tc_m(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, in
 }  // namespace tc
 
 // Orders routed to the tensor cores by default: measured faster than the
-// XOR+POPC kernels from m = 48 on (B200, 2.5e5 matrices: m = 48 8.2e8 vs
-// 6.4e8 evals/s, m = 64 5.2e8 vs 3.4e8; at m = 44 XOR+POPC wins, 9.8e8 vs
-// 8.3e8); HGA_FITNESS_TC=all routes every order 4..64, HGA_FITNESS_TC=0 none.
+// XOR+POPC kernels from m = 48 on (B200, 10^6 matrices, F2: m = 48 8.4e8 vs
+// 6.3e8 evals/s, m = 64 6.8e8 vs 3.7e8; at m = 44 XOR+POPC wins, 9.1e8 vs
+// 8.6e8); HGA_FITNESS_TC=all routes every order 4..64, HGA_FITNESS_TC=0 none.
 bool fit_tc_order(int m, bool all) { return (m % 4) == 0 && m >= (all ? 4 : 48) && m <= 64; }
 
 int launch_fit_tc(int m, const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth,

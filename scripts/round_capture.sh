@@ -14,6 +14,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_run_v3 -s 30 -c 1 -o $out/k_run \
     python bench.py --steps 40 --warmup 3 --no-sweep --no-cpu > $out/ncu_krun.log 2>&1; echo "ncu k_run rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_fit_i8_tc -s 2 -c 1 -o $out/fit_tc48 \
-    python scripts/prof_tc.py 48 > $out/ncu_tc.log 2>&1; echo "ncu tc rc=$?"
+    python scripts/prof_tc.py 48 1000000 > $out/ncu_tc.log 2>&1; echo "ncu tc rc=$?"
 timeout 900 python scripts/probe.py --only fitness > $out/fitness_sweep.jsonl 2> $out/fitness_sweep.err; echo "probe rc=$?"
 timeout 300 python scripts/phase_timing.py > $out/phase.jsonl 2>&1; echo "phase rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_fit_i8_tc -s 2 -c 1 -o $out/fit_tc64 \
+    python scripts/prof_tc.py 64 1000000 > $out/ncu_tc64.log 2>&1; echo "ncu tc64 rc=$?"
