@@ -19,8 +19,9 @@
 //     K steps) whose accumulators interleave in TMEM (the second at lane
 //     offset 16), so each of the four epilogue warps (one per TMEM lane
 //     quarter) gets 16 Gram rows of each matrix: the work is balanced for
-//     every order.  Eight accumulator slots (512 TMEM columns) and sixteen
-//     shared-memory stages keep loads, MMAs and epilogues overlapped.
+//     every order.  Units of kB = 4 pairs, two accumulator slots (512 TMEM
+//     columns) and 6 (K = 64) / 12 (K = 32) shared-memory stages keep loads,
+//     MMAs and epilogues overlapped.
 //   * Epilogue: tcgen05.ld 32x32b.x16 -> registers; each lane sums |g|,
 //     [g != 0] and g^2 over its row; 16-lane shuffles and a 4-warp combine
 //     give the matrix totals.
@@ -44,7 +45,15 @@ namespace tc {
 
 constexpr int kStageBytes = 192 * 1024;  // all stages; > 114 KB keeps one CTA (and one TMEM owner) per SM
 constexpr int kMaxStages = 48;
-constexpr int kB = 2;          // MMA pairs per pipeline unit (one barrier round trip per unit)
+#ifndef HGA_TC_KB
+#define HGA_TC_KB 4
+#endif
+// MMA pairs per pipeline unit (one barrier round trip per unit).  Measured
+// (B200, 10^6 matrices, F2): kB = 1 / 2 / 4 -> m = 48: 5.4 / 8.4 / 9.7e8,
+// m = 64: 4.4 / 6.7 / 7.7e8 evals/s -- the per-unit costs (mbarrier round
+// trips, group barrier, finalisation) dominate small units; kB = 4 leaves 2
+// accumulator slots of 256 TMEM columns, so 2 epilogue groups.
+constexpr int kB = HGA_TC_KB;
 constexpr int kSlotCols = kB * 64;
 constexpr int kSlots = 512 / kSlotCols;  // TMEM accumulator slots
 // epilogue groups of 4 warps (one per TMEM lane quarter); group g takes units it = g mod kEpiGroups.
@@ -253,16 +262,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
             const int s = it % G::STAGES;
             if (checker) {
-                // Check of one staged tile (check warp lw takes tile lw = pair lw / 2,
-                // interleave lw % 2): every byte of each matrix's rows < m and column
+                // Check of the staged tiles (check warp lw takes tiles lw, lw + 4, ..;
+                // tile tt = pair tt / 2, interleave tt % 2): every byte of each matrix's rows < m and column
                 // groups must be 0x00, 0x01 or 0xFF (entries in {-1, 0, +1}; padding is
                 // 0), and the nonzero bytes (bit 0 set) must number m^2 -- so no entry
                 // is 0.  16-byte chunks of the canonical layout, contiguous per lane
                 // group: conflict-free, independent of the loaders' piece order.
                 mbar_wait(&full[s], (it / G::STAGES) & 1);
-                if (!(flags & 8)) {
-                    const uint8_t* tile = smem + (size_t)(s * UT + lw) * G::TILE;
-                    const int b = lw >> 1;
+                for (int tt = lw; tt < ((flags & 8) ? 0 : UT); tt += kCheckWarps) {
+                    const uint8_t* tile = smem + (size_t)(s * UT + tt) * G::TILE;
+                    const int b = tt >> 1, j = tt & 1;
 #pragma unroll
                     for (int e = 0; e < G::P; ++e) {
                         uint32_t cnt = 0;

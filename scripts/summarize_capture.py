@@ -24,8 +24,8 @@ for a, b in (("bench.json", "bench.json"), ("bench_ref.json", "bench_ref.json"),
         shutil.copy(src / a, dst / f"{pre}_{b}")
 
 # launch list -> per-kernel totals
-rows = [r for r in csv.reader(open(src / "launches.csv")) if len(r) > 10]
-hdr = rows[0]
+rows = [r for r in csv.reader(open(src / "launches.csv")) if len(r) > 10] if (src / "launches.csv").exists() else []
+hdr = rows[0] if rows else ["Kernel Name", "Metric Name", "Metric Value"]
 ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
 agg = defaultdict(lambda: [0, 0.0])
 for r in rows[1:]:
@@ -37,7 +37,7 @@ for r in rows[1:]:
         agg[name][0] += 1
         agg[name][1] += us
 tot = sum(v[1] for v in agg.values())
-with open(dst / f"{pre}_bench_launches_summary.csv", "w") as f:
+with open(dst / f"{pre}_bench_launches_summary.csv" if rows else "/dev/null", "w") as f:
     f.write("kernel,launches,total_us,share\n")
     for k, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         f.write(f"{k},{n},{us:.1f},{us / tot:.3f}\n")
