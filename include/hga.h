@@ -56,6 +56,8 @@ extern "C" {
 #define HGA_FLAG_POINT_RANGE 2  /* crossover point outside [1, m-1] */
 #define HGA_FLAG_PLAN_RANGE 4   /* mutation plan index out of range */
 #define HGA_FLAG_FIT_RANGE 8    /* fitness range exceeds the select histogram */
+#define HGA_FLAG_NOT_GA 16      /* hga_pack_i8: column 0 is not all +1 or a column is
+                                   unbalanced (the GA invariants, engine.py:440-446) */
 
 /* mutation strategies (engine.py:58) */
 #define HGA_MUT_SHARED 0
@@ -69,6 +71,9 @@ int hga_probe(int32_t kind, int64_t iters, int32_t blocks, int32_t threads, uint
               void *stream);
 const char *hga_strerror(int rc);
 int hga_sm_count(int device);
+/* Clears (and returns) the calling thread's sticky-free CUDA error state
+ * (cudaGetLastError), e.g. after a failed cudaHostRegister by the host. */
+int hga_clear_last_error(void);
 
 /* ---------------------------------------------------------------- fitness */
 
@@ -90,7 +95,10 @@ int hga_fitness_i8(const int8_t *pop, int64_t n, int32_t m, uint32_t variants, i
 int hga_fitness_packed(const uint32_t *cols, int64_t n, int32_t m, uint32_t variants,
                        int64_t *f1, int64_t *f2, int64_t *orth, int64_t *sq, void *stream);
 
-/* int8 (n, m, m) <-> packed conversion (layout edge of the API). */
+/* int8 (n, m, m) <-> packed conversion (layout edge of the API).  The pack
+ * also ORs HGA_FLAG_NOT_GA into bad_flag when a matrix breaks the GA
+ * invariants (column 0 all +1, every other column balanced) -- the Philox
+ * generation loop's fast paths rely on them (engine.py:440-446). */
 int hga_pack_i8(const int8_t *pop, int64_t n, int32_t m, uint32_t *cols, int32_t *bad_flag,
                 void *stream);
 int hga_unpack_i8(const uint32_t *cols, int64_t n, int32_t m, int8_t *pop, void *stream);
@@ -239,8 +247,11 @@ int hga_run(const hga_run_args *args, void *stream);
  * dev_i8 is a device int8 staging buffer of 4N*m*m
  * bytes.  On return (copy_stream synchronised) host_pop/host_fit hold the new
  * population, state_out[0..7] the device state after the generation and
- * *flag_out the HGA_FLAG_* bits (HGA_FLAG_NOT_SIGN: an input entry was not
- * +-1). */
+ * *flag_out the HGA_FLAG_* bits.  The population is validated after the
+ * upload (one host synchronisation): when HGA_FLAG_NOT_SIGN (an entry is not
+ * +-1) or HGA_FLAG_NOT_GA (column 0 not all +1, or an unbalanced column) is
+ * set, nothing runs, host_pop/host_fit are left untouched and the caller
+ * takes the exact explicit-plan path instead. */
 int hga_step_host(const hga_run_args *args, int8_t *host_pop, int64_t *host_fit, int8_t *dev_i8,
                   const int64_t *state_in, int64_t *state_out, int32_t *flag_out, int32_t chunks,
                   void *stream, void *copy_stream);

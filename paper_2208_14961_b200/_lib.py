@@ -24,7 +24,7 @@ VAR_F1, VAR_F2, VAR_ORTH, VAR_SQ = 1, 2, 4, 8
 VAR_ALL = 15
 VARIANT_BITS = {"f1": VAR_F1, "f2": VAR_F2, "orth": VAR_ORTH, "sq": VAR_SQ}
 
-FLAG_NOT_SIGN, FLAG_POINT_RANGE, FLAG_PLAN_RANGE, FLAG_FIT_RANGE = 1, 2, 4, 8
+FLAG_NOT_SIGN, FLAG_POINT_RANGE, FLAG_PLAN_RANGE, FLAG_FIT_RANGE, FLAG_NOT_GA = 1, 2, 4, 8, 16
 
 RUN_FORCE = 1
 RUN_TIMING = 2
@@ -73,6 +73,7 @@ SIGNATURES = {
     "hga_probe": (_int, [_i32, _i64, _i32, _i32, _vp, _vp]),
     "hga_strerror": (ctypes.c_char_p, [_int]),
     "hga_sm_count": (_int, [_int]),
+    "hga_clear_last_error": (_int, []),
     "hga_fitness_i8_ws_bytes": (_sz, [_i64, _i32]),
     "hga_fitness_i8": (_int, [_vp, _i64, _i32, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "hga_fitness_packed": (_int, [_vp, _i64, _i32, _u32, _vp, _vp, _vp, _vp, _vp]),

@@ -175,25 +175,31 @@ __global__ void __launch_bounds__(kFitThreads)
 
 __global__ void k_pack_any(const int8_t* __restrict__ pop, int64_t n, int m, int W,
                            uint32_t* __restrict__ cols, int32_t* bad_flag) {
-    const int64_t total = n * m * W;
-    uint32_t bad = 0;
+    // thread per (matrix k, column j): neighbouring threads read neighbouring
+    // bytes of a row; the column's W words are built (and its popcount taken
+    // for the GA-invariant flag) in one walk down the rows
+    const int64_t total = n * m;
+    uint32_t bad = 0, not_ga = (m & 3) ? 1u : 0u;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int w = (int)(t % W);
-        const int64_t kj = t / W;
-        const int j = (int)(kj % m);
-        const int64_t k = kj / m;
-        const int8_t* p = pop + k * m * (int64_t)m + (int64_t)(32 * w) * m + j;
-        const int nr = min(32, m - 32 * w);
-        uint32_t word = 0;
-        for (int rr = 0; rr < nr; ++rr) {
-            int8_t b = p[(int64_t)rr * m];
-            bad |= (b != 1 && b != -1);
-            word |= ((uint32_t)(int32_t)b >> 31) << rr;
+        const int j = (int)(t % m);
+        const int8_t* p = pop + (t - j) * (int64_t)m + j;
+        int neg = 0;
+        for (int w = 0; w < W; ++w) {
+            const int nr = min(32, m - 32 * w);
+            uint32_t word = 0;
+            for (int rr = 0; rr < nr; ++rr) {
+                const int8_t b = p[(int64_t)(32 * w + rr) * m];
+                bad |= (b != 1 && b != -1);
+                word |= ((uint32_t)(int32_t)b >> 31) << rr;
+            }
+            cols[t * W + w] = word;
+            neg += __popc(word);
         }
-        cols[t] = word;
+        not_ga |= (uint32_t)(neg != (j == 0 ? 0 : m / 2));
     }
-    if (bad && bad_flag) atomicOr(bad_flag, HGA_FLAG_NOT_SIGN);
+    const uint32_t f = (bad ? HGA_FLAG_NOT_SIGN : 0u) | (not_ga ? HGA_FLAG_NOT_GA : 0u);
+    if (f && bad_flag) atomicOr(bad_flag, (int32_t)f);
 }
 
 __global__ void k_fitness_any(const uint32_t* __restrict__ cols, int64_t n, int m, int W,
@@ -246,13 +252,14 @@ __global__ void k_unpack(const uint32_t* __restrict__ cols, int64_t n, int m, in
 // Pack for m % 4 == 0, m <= 64: thread (matrix k, column quad jq) walks the
 // rows with one 4-byte load each (consecutive threads read consecutive
 // quads of a row), collects the four columns' sign bits and checks the bytes
-// are +-1 (byte ^ 1 has bit 0 clear and bits 1..7 equal).
+// are +-1 (byte ^ 1 has bit 0 clear and bits 1..7 equal) and the columns
+// keep the GA invariants (popcount 0 for column 0, m / 2 for the others).
 template <int W>
 __global__ void k_pack_quads(const int8_t* __restrict__ pop, int64_t n, int m, uint32_t* __restrict__ cols,
                              int32_t* bad_flag) {
     const int q4 = m >> 2;
     const int64_t quads = n * q4;
-    uint32_t bad = 0;
+    uint32_t bad = 0, not_ga = 0;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < quads; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = t / q4;
         const int jq = (int)(t - k * q4);
@@ -275,11 +282,18 @@ __global__ void k_pack_quads(const int8_t* __restrict__ pop, int64_t n, int m, u
         }
         uint32_t* out = cols + (k * m + 4 * jq) * W;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 4; ++c) {
+            int neg = 0;
 #pragma unroll
-            for (int x = 0; x < W; ++x) out[c * W + x] = w[c][x];
+            for (int x = 0; x < W; ++x) {
+                out[c * W + x] = w[c][x];
+                neg += __popc(w[c][x]);
+            }
+            not_ga |= (uint32_t)(neg != ((jq | c) == 0 ? 0 : (m >> 1)));
+        }
     }
-    if (bad && bad_flag) atomicOr(bad_flag, HGA_FLAG_NOT_SIGN);
+    const uint32_t f = (bad ? HGA_FLAG_NOT_SIGN : 0u) | (not_ga ? HGA_FLAG_NOT_GA : 0u);
+    if (f && bad_flag) atomicOr(bad_flag, (int32_t)f);
 }
 
 // Row-at-a-time unpack for m % 4 == 0: thread (matrix k, row r) reads row
@@ -411,7 +425,7 @@ int hga_fitness_i8(const int8_t* pop, int64_t n, int32_t m, uint32_t variants, i
     uint32_t* cols = (uint32_t*)ws;
     for (int64_t k0 = 0; k0 < n; k0 += chunk) {
         const int64_t c = std::min(chunk, n - k0);
-        k_pack_any<<<grid_for(c * m * W, 256), 256, 0, st>>>(pop + k0 * m * (int64_t)m, c, m, W, cols, bad_flag);
+        k_pack_any<<<grid_for(c * m, 256), 256, 0, st>>>(pop + k0 * m * (int64_t)m, c, m, W, cols, bad_flag);
         k_fitness_any<<<(unsigned)std::min<int64_t>(c, sm_count_cached() * 8), 128, 0, st>>>(
             cols, c, m, W, variants, k0, f1, f2, orth, sq);
     }
@@ -443,7 +457,7 @@ int hga_pack_i8(const int8_t* pop, int64_t n, int32_t m, uint32_t* cols, int32_t
         if (W == 1) k_pack_quads<1><<<g, 256, 0, st>>>(pop, n, m, cols, bad_flag);
         else k_pack_quads<2><<<g, 256, 0, st>>>(pop, n, m, cols, bad_flag);
     } else {
-        k_pack_any<<<grid_for(n * m * W, 256), 256, 0, st>>>(pop, n, m, W, cols, bad_flag);
+        k_pack_any<<<grid_for(n * m, 256), 256, 0, st>>>(pop, n, m, W, cols, bad_flag);
     }
     return to_rc(cudaGetLastError());
 }
@@ -459,6 +473,8 @@ int hga_unpack_i8(const uint32_t* cols, int64_t n, int32_t m, int8_t* pop, void*
 }
 
 int hga_abi_version(void) { return HGA_ABI_VERSION; }
+
+int hga_clear_last_error(void) { return (int)cudaGetLastError(); }
 
 int hga_sm_count(int device) {
     int v = 0;

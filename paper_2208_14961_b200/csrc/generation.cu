@@ -811,6 +811,14 @@ int hga_step_host(const hga_run_args* a, int8_t* host_pop, int64_t* host_fit, in
         if (rc) return done(rc);
     }
     if (e != cudaSuccess) return done(to_rc(e));
+    // validate before anything is computed: the loop's fast paths need the GA
+    // invariants (column 0 skipped in the pair chain, fitness >> granule keys);
+    // on a violation the host arrays stay untouched and the caller runs the
+    // exact explicit-plan generation instead
+    e = cudaMemcpyAsync(flag_out, dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return done(to_rc(e));
+    if (*flag_out & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA)) return HGA_OK;
     if (tm) cudaEventRecord(te[1], cs);
     if (tm) cudaEventRecord(te[2], st);
     k_set_state<<<1, 8, 0, st>>>(a->state, state_in[0], state_in[1], state_in[2], state_in[6], state_in[7]);

@@ -37,8 +37,8 @@ import torch
 
 from . import _dev
 from ._dev import HgaError, check, lib, ptr, stream_ptr, words_for
-from ._lib import (FLAG_FIT_RANGE, FLAG_NOT_SIGN, FLAG_PLAN_RANGE, FLAG_POINT_RANGE, MUT_CODES, RUN_FORCE, RunArgs,
-                   VARIANT_BITS)
+from ._lib import (FLAG_FIT_RANGE, FLAG_NOT_GA, FLAG_NOT_SIGN, FLAG_PLAN_RANGE, FLAG_POINT_RANGE, MUT_CODES, RUN_FORCE,
+                   RunArgs, VARIANT_BITS)
 from .rand import MASK64, RngStream, random_seed
 
 __all__ = [
@@ -693,18 +693,24 @@ def step(state, workers: int = 1):
     return state
 
 
+def _host_config(cfg) -> GAConfig:
+    """Our GAConfig for a host state's config (ours or the reference's)."""
+    if isinstance(cfg, GAConfig):
+        return cfg
+    return GAConfig(order=cfg.order, population=cfg.population, max_iterations=cfg.max_iterations,
+                    mutation_cols=cfg.mutation_cols, mutation_row_pairs=cfg.mutation_row_pairs, fitness=cfg.fitness,
+                    mutation=cfg.mutation, seed=cfg.seed, stall_window=cfg.stall_window,
+                    time_budget_secs=cfg.time_budget_secs, rng=getattr(cfg, "rng", "reference"))
+
+
 class _HostBridge:
     """Device buffers behind a host (numpy) search state; host arrays are
-    page-locked in place (cudaHostRegister) so the per-step copies are DMA."""
+    page-locked in place (cudaHostRegister) so the per-step copies are DMA.
+    Rebuilt whenever the state's config or seed changes (`key`)."""
 
-    def __init__(self, state):
-        cfg = state.config
-        rng = getattr(cfg, "rng", "reference")
-        self.cfg = cfg if isinstance(cfg, GAConfig) else GAConfig(
-            order=cfg.order, population=cfg.population, max_iterations=cfg.max_iterations,
-            mutation_cols=cfg.mutation_cols, mutation_row_pairs=cfg.mutation_row_pairs, fitness=cfg.fitness,
-            mutation=cfg.mutation, seed=cfg.seed, stall_window=cfg.stall_window,
-            time_budget_secs=cfg.time_budget_secs, rng=rng)
+    def __init__(self, state, cfg: GAConfig, key: tuple):
+        self.cfg = cfg
+        self.key = key
         self.res = _Resident(self.cfg, int(state.seed) & MASK64)
         m, total = self.cfg.order, self.cfg.total
         self.pop_i8 = torch.empty((total, m, m), dtype=torch.int8, device=self.res.dev)
@@ -720,15 +726,25 @@ class _HostBridge:
         self.args = None
 
     def pin(self, arr: np.ndarray) -> None:
-        held = self.registered.get(arr.ctypes.data)
+        """Page-lock `arr` in place; not fatal when the runtime refuses (already
+        pinned or registered memory, overlapping ranges): the copies then go
+        through the driver's staging path and the error state is cleared."""
+        addr = arr.ctypes.data
+        held = self.registered.get(addr)
         if arr.nbytes == 0 or (held is not None and held.nbytes >= arr.nbytes):
             return
-        rt = torch.cuda.cudart()
-        rc = rt.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
-        if int(rc) == 0:
-            self.registered[arr.ctypes.data] = arr
+        try:
+            rt = torch.cuda.cudart()
+            if held is not None:  # same address, larger array: re-register the whole range
+                rt.cudaHostUnregister(addr)
+                del self.registered[addr]
+            rc = int(rt.cudaHostRegister(addr, arr.nbytes, 0))
+        except Exception:  # noqa: BLE001 -- registration is an optimisation only
+            rc = -1
+        if rc == 0:
+            self.registered[addr] = arr
         else:
-            rt.cudaGetLastError()  # not fatal: the copies go through pageable staging instead
+            lib.hga_clear_last_error()
 
 
 def _unregister_all(registered: dict) -> None:
@@ -736,7 +752,7 @@ def _unregister_all(registered: dict) -> None:
         rt = torch.cuda.cudart()
         for addr in list(registered):
             rt.cudaHostUnregister(addr)
-        rt.cudaGetLastError()
+        lib.hga_clear_last_error()
     except Exception:  # noqa: BLE001 -- interpreter shutdown
         pass
     registered.clear()
@@ -750,28 +766,59 @@ def _chunks(total: int) -> list[tuple[int, int]]:
     return [(total * i // k, total * (i + 1) // k) for i in range(k)]
 
 
+def _bridge_for(state) -> _HostBridge:
+    cfg = _host_config(state.config)
+    key = (cfg.order, cfg.population, cfg.mutation_cols, cfg.mutation_row_pairs, cfg.fitness, cfg.mutation,
+           cfg.stall_window, cfg.rng, int(state.seed) & MASK64)
+    bridge = getattr(state, "_hga_bridge", None)
+    if bridge is None or bridge.key != key:
+        bridge = _HostBridge(state, cfg, key)
+        state._hga_bridge = bridge
+    return bridge
+
+
+def _host_arrays(state, cfg: GAConfig):
+    """(population, fitness) as C-contiguous int8 / int64 arrays of the
+    config's shapes: the caller's own arrays when they already are, else
+    scratch copies that are written back (with the caller's dtype) after
+    the step -- the native step reads and writes exactly these sizes."""
+    pop, fit = state.population, state.fitness
+    m, total = cfg.order, cfg.total
+    if not isinstance(pop, np.ndarray) or not isinstance(fit, np.ndarray):
+        raise ValueError("host state population and fitness must be numpy arrays")
+    if pop.shape != (total, m, m):
+        raise ValueError(f"population shape {pop.shape} does not match the config ({total}, {m}, {m})")
+    if fit.shape != (total,):
+        raise ValueError(f"fitness shape {fit.shape} does not match the config ({total},)")
+    p = pop if (pop.dtype == np.int8 and pop.flags.c_contiguous) else np.ascontiguousarray(pop, dtype=np.int8)
+    f = fit if (fit.dtype == np.int64 and fit.flags.c_contiguous) else np.ascontiguousarray(fit, dtype=np.int64)
+    if p is not pop and not np.array_equal(p, pop):
+        raise ValueError("step: matrix entries must be +1 or -1")
+    return p, f
+
+
 def _step_host(state):
     """One generation on a host (numpy) state, in place (engine.py:449-469).
 
     The int8 population goes up and comes back every step (the caller owns
     the arrays); the copies run on a side stream in chunks, each chunk packed
     (unpacked) on the compute stream as soon as it has landed (before it
-    leaves), and in Philox mode the only host synchronisation is the final one.
+    leaves), and in Philox mode the only host synchronisations are the
+    validation after the upload and the final one.  A population that breaks
+    the GA invariants (column 0 all +1, balanced columns) is stepped exactly
+    by the explicit-plan generation (all column pairs, exact keys) instead of
+    the Philox loop, whose fast paths rely on them.
     """
-    bridge = getattr(state, "_hga_bridge", None)
-    if bridge is None:
-        bridge = _HostBridge(state)
-        state._hga_bridge = bridge
-    pop_np, fit_np = state.population, state.fitness
-    if not (pop_np.flags.c_contiguous and fit_np.flags.c_contiguous):
-        raise ValueError("host population and fitness must be C-contiguous")
+    bridge = _bridge_for(state)
+    pop_np, fit_np = _host_arrays(state, bridge.cfg)
     bridge.pin(pop_np)
     bridge.pin(fit_np)
-    res, inner = bridge.res, bridge.inner
-    res.cur = cur = 0  # the host arrays are authoritative: upload into buffer 0
+    res = bridge.res
+    res.cur = 0  # the host arrays are authoritative: upload into buffer 0
     it0, best0 = int(state.iteration), int(state.best_fitness)
     last0 = int(state.trace[-1]) if state.trace else best0
-    if bridge.cfg.rng == "philox" and res.m <= 64:
+    explicit = bridge.cfg.rng != "philox"
+    if not explicit and res.m <= 64:
         # the whole step is enqueued natively (hga_step_host): chunked copies on a
         # side stream overlapped with pack / unpack, one synchronisation at the end
         if bridge.args is None:  # the trace buffer is not used by this path; args stay valid
@@ -783,11 +830,31 @@ def _step_host(state):
         check(lib.hga_step_host(bridge.args, pop_np.ctypes.data, fit_np.ctypes.data, bridge.pop_i8.data_ptr(), st_in,
                                 bridge.host_state.data_ptr(), bridge.host_flag.data_ptr(), _HOST_CHUNKS,
                                 stream_ptr(), bridge.copy_stream.cuda_stream), "hga_step_host")
-        res.cur = 1
-        if int(bridge.hf_np[0]) & FLAG_NOT_SIGN:
+        hf = int(bridge.hf_np[0])
+        if hf & FLAG_NOT_SIGN:
             raise ValueError("step: matrix entries must be +1 or -1")
-        _finish_host_step(state, pop_np, fit_np, int(bridge.hs_np[0]), int(bridge.hs_np[7]))
-        return state
+        if not hf & FLAG_NOT_GA:
+            res.cur = 1
+            _finish_host_step(state, pop_np, fit_np, int(bridge.hs_np[0]), int(bridge.hs_np[7]))
+            _write_back(state, pop_np, fit_np)
+            return state
+        explicit = True  # host arrays untouched: take the exact path below
+    _step_host_generic(state, bridge, pop_np, fit_np, it0, best0, last0, explicit)
+    _write_back(state, pop_np, fit_np)
+    return state
+
+
+def _write_back(state, pop_np: np.ndarray, fit_np: np.ndarray) -> None:
+    if state.population is not pop_np:
+        state.population[...] = pop_np
+    if state.fitness is not fit_np:
+        state.fitness[...] = fit_np
+
+
+def _step_host_generic(state, bridge: _HostBridge, pop_np, fit_np, it0: int, best0: int, last0: int,
+                       explicit: bool) -> None:
+    res, inner = bridge.res, bridge.inner
+    cur = 0
     flag = _dev.new_flag()
     m, total, mw = res.m, 4 * res.N, res.mw
     comp, cs = torch.cuda.current_stream(), bridge.copy_stream
@@ -805,9 +872,20 @@ def _step_host(state):
         check(lib.hga_pack_i8(bridge.pop_i8[a].data_ptr(), b - a, m, res.pop[cur][a * mw].data_ptr(),
                               flag.data_ptr(), comp.cuda_stream), "hga_pack_i8")
     comp.wait_stream(cs)
-    bridge.host_state_in.copy_(torch.tensor([it0, best0, 0, cur, 0, 0, 1, last0], dtype=torch.int64))
-    res.dstate.copy_(bridge.host_state_in, non_blocking=True)
-    if bridge.cfg.rng == "philox":
+    # validate before anything is written back (the host arrays are in-place outputs)
+    fl = int(flag.item())
+    if fl & FLAG_NOT_SIGN:
+        raise ValueError("step: matrix entries must be +1 or -1")
+    if fl & FLAG_NOT_GA:
+        explicit = True
+    res.cur = cur
+    if explicit:
+        inner.iteration, inner.best_fitness, inner.trace, inner.best_matrix = it0, best0, [last0], None
+        _step_reference(inner)
+        new = res.cur
+    else:
+        bridge.host_state_in.copy_(torch.tensor([it0, best0, 0, cur, 0, 0, 1, last0], dtype=torch.int64))
+        res.dstate.copy_(bridge.host_state_in, non_blocking=True)
         check(lib.hga_run_prepare(res.run_args(), stream_ptr()), "hga_run_prepare")
         res.ensure_trace(it0 + 1)
         args = res.run_args()
@@ -815,10 +893,6 @@ def _step_host(state):
         args.flags |= RUN_FORCE  # exactly one generation: the new population is in buffer cur ^ 1
         check(lib.hga_run(args, stream_ptr()), "hga_run")
         new = cur ^ 1
-    else:
-        inner.iteration, inner.best_fitness, inner.trace, inner.best_matrix = it0, best0, [last0], None
-        step(inner)
-        new = res.cur
     for a, b in parts:
         check(lib.hga_unpack_i8(res.pop[new][a * mw].data_ptr(), b - a, m, bridge.pop_i8[a].data_ptr(),
                                 comp.cuda_stream), "hga_unpack_i8")
@@ -832,13 +906,11 @@ def _step_host(state):
         fit_t.copy_(res.fit[new], non_blocking=True)
         bridge.host_state.copy_(res.dstate, non_blocking=True)
     cs.synchronize()
-    _check_flag(flag, "step")
-    if bridge.cfg.rng == "philox":
-        it1, fmin = int(bridge.host_state[0]), int(bridge.host_state[7])
-    else:
+    if explicit:
         it1, fmin = inner.iteration, inner.trace[-1]
+    else:
+        it1, fmin = int(bridge.host_state[0]), int(bridge.host_state[7])
     _finish_host_step(state, pop_np, fit_np, it1, fmin)
-    return state
 
 
 def _finish_host_step(state, pop_np: np.ndarray, fit_np: np.ndarray, it1: int, fmin: int) -> None:

@@ -27,7 +27,7 @@ import torch.distributed as dist
 
 from . import _dev
 from ._dev import check, lib, stream_ptr
-from .engine import GAConfig, initial_state, _run_device, _best_from_packed
+from .engine import GAConfig, initial_state, _run_device, _best_from_packed, _sync_from_device
 from .rand import MASK64, mix64
 
 __all__ = ["IslandConfig", "Exchange", "GpuIsland", "IslandRecord", "island_seed", "run_islands",
@@ -67,6 +67,23 @@ class Exchange:
         t = torch.tensor([best, 0 if want_stop else 1], dtype=torch.int64, device=self.device)
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
         v = t.cpu().tolist()
+        return int(v[0]), v[1] == 0
+
+    def agree_tensor(self, best: torch.Tensor, want_stop: bool) -> torch.Tensor:
+        """Enqueue the agreement on a 1-element int64 `best` tensor (device
+        resident for NCCL: no host read before the collective) and return
+        the reduced (best, continue) pair without reading it; the caller's
+        next stream synchronisation covers it."""
+        flag = torch.ones(1, dtype=torch.int64, device=best.device) if not want_stop else \
+            torch.zeros(1, dtype=torch.int64, device=best.device)
+        t = torch.cat([best.reshape(1).to(torch.int64), flag]).to(self.device)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return t
+
+    @staticmethod
+    def read(t: torch.Tensor) -> tuple[int, bool]:
+        v = t.tolist()
         return int(v[0]), v[1] == 0
 
     def ring_shift(self, payload: torch.Tensor) -> torch.Tensor:
@@ -114,6 +131,7 @@ class GpuIsland:
         self.state = initial_state(config, seed=seed)
         self.res = self.state._res
         self._ws = None
+        self.last_received = None  # slots the last migrants were written to (tests)
 
     @property
     def iteration(self) -> int:
@@ -125,6 +143,22 @@ class GpuIsland:
 
     def advance(self, gens: int) -> None:
         _run_device(self.state, gens)
+
+    def launch(self, gens: int) -> None:
+        """Enqueue `gens` generations (one persistent launch), no host sync."""
+        res, st = self.res, self.state
+        res.ensure_trace(st.iteration + gens)
+        a = res.run_args()
+        a.gens_this_call = gens
+        check(lib.hga_run(a, stream_ptr()), "hga_run")
+
+    def best_tensor(self) -> torch.Tensor:
+        """Device-resident best-so-far fitness (state word 1)."""
+        return self.res.dstate[1:2]
+
+    def sync(self) -> None:
+        """Refresh the host view (best, iteration) from the device state."""
+        _sync_from_device(self.state)
 
     def elites(self, e: int) -> tuple[torch.Tensor, torch.Tensor]:
         """The e best individuals (lowest fitness, lowest index first) of the current population."""
@@ -147,23 +181,37 @@ class GpuIsland:
         return rec[:e], fit[:e]
 
     def receive(self, rec: torch.Tensor, fit: torch.Tensor) -> None:
-        """Migrants overwrite offspring slots [2N, 2N + e) of the current population."""
+        """Migrants overwrite the e WORST individuals of the current population
+        (largest fitness, lowest index first among equals), so the island's
+        own best always survives and its min fitness never rises; they then
+        compete in the next selection.  Everything stays on the device (no
+        host synchronisation): the selection histogram is rebuilt and the
+        loop's best-so-far (state word 1 + best matrix) takes a better
+        migrant, which the host sees at the next poll."""
         res = self.res
         e = rec.shape[0]
         if e == 0:
             return
-        half, cur, mw = 2 * res.N, res.cur, res.mw
-        res.pop[cur][half * mw:(half + e) * mw].copy_(rec.reshape(-1).to(res.dev))
-        res.fit[cur][half:half + e].copy_(fit.to(res.dev))
+        total, cur, mw = 4 * res.N, res.cur, res.mw
+        if e >= total:
+            raise ValueError("migration_size must be smaller than the island population")
+        rec = rec.reshape(e, mw).to(device=res.dev, dtype=torch.int32)
+        fit = fit.to(device=res.dev, dtype=torch.int64)
+        if self._ws is None:
+            self._ws = torch.empty(int(lib.hga_select_ws_bytes(total)), dtype=torch.uint8, device=res.dev)
+        neg = torch.neg(res.fit[cur])
+        worst = torch.empty(e, dtype=torch.int64, device=res.dev)
+        flag = _dev.new_flag()
+        check(lib.hga_select_smallest(neg.data_ptr(), total, e, worst.data_ptr(), flag.data_ptr(),
+                                      self._ws.data_ptr(), self._ws.shape[0], stream_ptr()), "hga_select_smallest")
+        res.pop[cur].view(total, mw).index_copy_(0, worst, rec)
+        res.fit[cur].index_copy_(0, worst, fit)
         check(lib.hga_run_prepare(res.run_args(), stream_ptr()), "hga_run_prepare")
-        best_in = int(fit.min().item())
-        if best_in < self.state.best_fitness:
-            # keep the device loop's best-so-far consistent with the population
-            k = int(fit.argmin().item())
-            self.state.best_fitness = best_in
-            res.best_packed.copy_(rec[k].reshape(-1).to(res.dev))
-            self.state.best_matrix = _best_from_packed(res, res.best_packed)
-            res.dstate[1] = best_in
+        k = torch.argmin(fit)
+        better = fit[k] < res.dstate[1]
+        res.best_packed.copy_(torch.where(better, rec[k], res.best_packed))
+        res.dstate[1:2].copy_(torch.minimum(res.dstate[1:2], fit[k].reshape(1)))
+        self.last_received = worst
 
     def best_matrix_packed(self) -> torch.Tensor:
         return self.res.best_packed
@@ -201,14 +249,22 @@ def run_islands(config: GAConfig, island_config: IslandConfig = IslandConfig(), 
     complete = True
     best, _ = ex.agree(island.best, False)
     trace = [best]
+    pipelined = hasattr(island, "launch")
     while True:
         if best == 0 or island.iteration >= config.max_iterations:
             break
         to_mig = ic.migration_interval - (island.iteration % ic.migration_interval)
         gens = min(ic.poll_interval, to_mig, config.max_iterations - island.iteration)
-        island.advance(gens)
         over = config.time_budget_secs is not None and time.perf_counter() - start > config.time_budget_secs
-        best, stop = ex.agree(island.best, over)
+        if pipelined:
+            # launch, agree on the device-resident best, then ONE host sync per poll
+            island.launch(gens)
+            t = ex.agree_tensor(island.best_tensor(), over)
+            island.sync()
+            best, stop = ex.read(t)
+        else:
+            island.advance(gens)
+            best, stop = ex.agree(island.best, over)
         trace.append(best)
         if stop:
             complete = best == 0
@@ -220,6 +276,8 @@ def run_islands(config: GAConfig, island_config: IslandConfig = IslandConfig(), 
             r2, f2 = unpack_payload(incoming, e, rec.shape[1])
             island.receive(r2, f2)
             migrations += 1
+    if pipelined:
+        island.sync()  # migrants received after the last poll may hold the best
     owner = ex.owner_of_best(island.best)
     mat = ex.broadcast(island.best_matrix_packed().reshape(-1).to(torch.int32), owner)
     if isinstance(island, GpuIsland):
@@ -243,34 +301,49 @@ def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
-def evaluate_sharded(population, fitness: str = "f2", group=None, evaluator=None):
+def evaluate_sharded(population, fitness: str = "f2", group=None, evaluator=None, local: bool = False):
     """`evaluate` across all ranks of a torch.distributed job: rank r scores
-    its contiguous slice on its own GPU and one all_gather returns the whole
-    fitness vector (int64, numpy) on every rank; no other collective.
+    only its contiguous slice on its own GPU and one all_gather returns the
+    whole fitness vector on every rank; no other collective.
 
-    Every rank passes the same population (numpy or a tensor); `evaluator`
-    replaces the GPU kernel (tests run the protocol on gloo with the CPU
-    oracle).  Without an initialised process group this is `evaluate`.
+    * `local=False`: every rank passes the same population (numpy or a
+      tensor) and scores `population[lo:hi]` (`shard_bounds`); only that
+      slice is copied to the device.
+    * `local=True`: each rank passes ONLY its own slice (config 5 at 10^7
+      matrices need not exist on any one host); the slice sizes are agreed
+      with one extra 8-byte all_gather.
+    With NCCL the gather runs on device tensors (no host staging); the
+    result is a CUDA int64 tensor for tensor input and numpy for numpy
+    input.  `evaluator(pop, fitness)` replaces the GPU kernel (the CPU tests
+    run the protocol on gloo with the oracle).  Without an initialised
+    process group this is `evaluate`.
     """
     from . import engine
 
-    evaluator = evaluator or (lambda pop, fit: np.asarray(engine.evaluate(pop, fit)))
+    host_in = not isinstance(population, torch.Tensor)
+    evaluator = evaluator or engine.evaluate
     if not (dist.is_available() and dist.is_initialized()):
         return evaluator(population, fitness)
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    n = int(population.shape[0])
-    lo, hi = shard_bounds(n, world, rank)
-    mine = evaluator(population[lo:hi], fitness)
-    mine = torch.as_tensor(np.asarray(mine, dtype=np.int64))
-    width = -(-n // world)  # all_gather needs equal sizes: pad every slice to the largest
-    buf = torch.zeros(width, dtype=torch.int64)
-    buf[: hi - lo] = mine
-    if dist.get_backend(group) == "nccl":
-        buf = buf.cuda()
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    if local:
+        mine_pop = population
+        cnt = torch.tensor([int(population.shape[0])], dtype=torch.int64, device=dev)
+        counts = [torch.empty_like(cnt) for _ in range(world)]
+        dist.all_gather(counts, cnt, group=group)
+        sizes = [int(c.item()) for c in counts]
+    else:
+        n = int(population.shape[0])
+        sizes = [shard_bounds(n, world, r)[1] - shard_bounds(n, world, r)[0] for r in range(world)]
+        lo, hi = shard_bounds(n, world, rank)
+        mine_pop = population[lo:hi]
+    mine = evaluator(mine_pop, fitness)
+    mine = torch.as_tensor(mine).to(device=dev, dtype=torch.int64)
+    width = max(max(sizes), 1)  # all_gather needs equal sizes: pad every slice to the largest
+    buf = torch.zeros(width, dtype=torch.int64, device=dev)
+    buf[: mine.shape[0]] = mine
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf, group=group)
-    out = np.empty(n, dtype=np.int64)
-    for r, part in enumerate(parts):
-        a, b = shard_bounds(n, world, r)
-        out[a:b] = part[: b - a].cpu().numpy()
-    return out
+    out = torch.cat([part[:sz] for part, sz in zip(parts, sizes)])
+    return out.cpu().numpy() if host_in else out.to(population.device)

@@ -79,10 +79,12 @@ class HostIsland:
         return torch.from_numpy(pack_np(self.st.population[order])), torch.from_numpy(self.st.fitness[order].copy())
 
     def receive(self, rec, fit):
+        # same rule as GpuIsland.receive: migrants replace the e worst (largest
+        # fitness, lowest index first among equals)
         e = rec.shape[0]
-        half = 2 * self.cfg.population
-        self.st.population[half:half + e] = unpack_np(rec.numpy(), self.cfg.order)
-        self.st.fitness[half:half + e] = fit.numpy()
+        worst = np.argsort(-self.st.fitness, kind="stable")[:e]
+        self.st.population[worst] = unpack_np(rec.numpy(), self.cfg.order)
+        self.st.fitness[worst] = fit.numpy()
         self.received += e
         b = int(self.st.fitness.min())
         if b < self.st.best_fitness:
@@ -170,7 +172,12 @@ def _shard_worker(rank, world, port, q):
             return oracle.evaluate(p, fit)
 
         got = evaluate_sharded(pop, "f1", evaluator=ev)
-        q.put((rank, got.tolist(), seen, shard_bounds(len(pop), world, rank)))
+        lo, hi = shard_bounds(len(pop), world, rank)
+        # local mode: each rank holds only its own (uneven) slice
+        cut = [0, 100, 101, 1004]
+        got_local = evaluate_sharded(pop[cut[rank]:cut[rank + 1]], "f1", evaluator=ev, local=True)
+        t = evaluate_sharded(torch.from_numpy(pop), "f1", evaluator=lambda p, f: oracle.evaluate(p.numpy(), f))
+        q.put((rank, got.tolist(), seen, (lo, hi), got_local.tolist(), t.tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -193,8 +200,9 @@ def test_sharded_fitness_gloo():
         assert p.exitcode == 0
     want = oracle.evaluate(oracle.init_population(12, 251, 3), "f1").tolist()
     bounds = []
-    for rank, got, seen, (lo, hi) in res:
+    for rank, got, seen, (lo, hi), got_local, t in res:
         assert got == want, rank
-        assert seen == [hi - lo]
+        assert got_local == want and t == want, rank
+        assert seen == [hi - lo, [100, 1, 903][rank]]
         bounds.append((lo, hi))
     assert bounds == [(0, 334), (334, 669), (669, 1004)]
