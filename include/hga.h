@@ -65,8 +65,11 @@ extern "C" {
 #define HGA_MUT_MULTI 2
 
 int hga_abi_version(void);
-/* pipe-rate microbenchmark: kind 0 = XOR+POPC chains, 1 = LOP3+IADD chains;
- * each thread runs iters * 8 operations. */
+/* pipe-rate microbenchmark: kind 0 = XOR+POPC chains, 1 = LOP3+IADD chains
+ * (each thread runs iters * 8 operations); kind 2 / 3 = dense int8
+ * tcgen05.mma (s8 x s8 -> s32) of shape 128 x 256 x 32 / 64 x 64 x 32, iters
+ * instructions issued back to back by one thread per CTA (one CTA per SM;
+ * `threads` ignored; ops = blocks * iters * 2 * M * N * 32). */
 int hga_probe(int32_t kind, int64_t iters, int32_t blocks, int32_t threads, uint32_t *out,
               void *stream);
 const char *hga_strerror(int rc);

@@ -24,13 +24,26 @@ HGA_V2_ORDERS(HGA_V2_EXTERN)
 bool fit_tc_order(int m, bool all);
 int launch_fit_tc(int m, const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth,
                   int64_t* sq, int32_t* bad, cudaStream_t st);
+// round-2 tensor-core kernel (fitness_tc2.cu), orders 36..64
+bool fit_tc2_order(int m);
+int launch_fit_tc2(int m, const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t* f2, int64_t* orth,
+                   int64_t* sq, int32_t* bad, cudaStream_t st);
 // HGA_FITNESS_TC=0 selects the XOR+POPC kernels at every order, =all the
-// tensor cores at every order 4..64 (cross-checks, A/B timing)
-static int fit_tc_mode() {
+// round-1 tensor-core kernel at every order 4..64, =v1 the round-1 kernel at
+// its default orders (48..64), =2 the round-2 kernel at every order 36..64
+// (cross-checks, A/B timing); default: the round-2 kernel from order
+// HGA_TC2_MIN (default 44) to 64
+static int fit_tc_mode() {  // read per call: tests and sweeps switch it at run time
     const char* e = std::getenv("HGA_FITNESS_TC");
     if (e && e[0] == '0') return 0;
     if (e && e[0] == 'a') return 2;
+    if (e && e[0] == 'v') return 3;
+    if (e && e[0] == '2') return 4;
     return 1;
+}
+static int tc2_min_order() {
+    const char* e = std::getenv("HGA_TC2_MIN");
+    return e ? std::atoi(e) : 44;
 }
 
 static int launch_fit_v2(int m, bool from_i8, const void* src, int64_t n, uint32_t v, int64_t* f1, int64_t* f2,
@@ -413,7 +426,10 @@ int hga_fitness_i8(const int8_t* pop, int64_t n, int32_t m, uint32_t variants, i
     if (n == 0) return HGA_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int tc_mode = fit_tc_mode();
-    if (tc_mode && fit_tc_order(m, tc_mode == 2) && (((uintptr_t)pop) & 15) == 0)
+    const bool al16 = (((uintptr_t)pop) & 15) == 0;
+    if (((tc_mode == 1 && m >= tc2_min_order()) || tc_mode == 4) && al16 && fit_tc2_order(m))
+        return launch_fit_tc2(m, pop, n, variants, f1, f2, orth, sq, bad_flag, st);
+    if ((tc_mode == 2 || tc_mode == 3) && al16 && fit_tc_order(m, tc_mode == 2))
         return launch_fit_tc(m, pop, n, variants, f1, f2, orth, sq, bad_flag, st);
     if (v2_order(m) && (((uintptr_t)pop) & 15) == 0)
         return launch_fit_v2(m, true, pop, n, variants, f1, f2, orth, sq, bad_flag, st);

@@ -2,6 +2,7 @@
 // ceiling the fitness kernels are measured against (SURVEY.md section 8d
 // flags the POPC rate as an assumption to be measured on the box).
 #include "hga_common.cuh"
+#include "tcgen05.cuh"
 
 namespace hga {
 
@@ -41,14 +42,79 @@ __global__ void k_probe_alu(int64_t iters, uint32_t seed, uint32_t* out) {
     if (s == 0xFFFFFFFFu) out[blockIdx.x] = s;
 }
 
+// Dense int8 tensor-core rate: one elected thread per CTA issues `iters`
+// back-to-back tcgen05.mma.kind::i8 (s8 x s8 -> s32) of shape M x N x 32 from
+// shared memory into two TMEM accumulators (MN-major no-swizzle operands, the
+// fitness kernels' layout), then waits for the last one.  ops = iters * 2MNK.
+// (M, N) = (128, 256): the largest single-CTA shape (the pipe's dense peak);
+// (64, 64): the fitness kernels' own shape (M = 64 runs half the datapath).
+template <int M, int N>
+__global__ void __launch_bounds__(128, 1) k_probe_mma_i8(int64_t iters, uint32_t* out) {
+    using namespace tcx;
+    extern __shared__ __align__(1024) uint8_t smem[];  // A: M x 32 bytes, B: N x 32 bytes
+    __shared__ __align__(8) uint64_t done;
+    __shared__ uint32_t tmem_base;
+    constexpr int ABYTES = M * 32, BBYTES = N * 32;
+    for (int i = threadIdx.x; i < (ABYTES + BBYTES) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(smem)[i] = 0x01FF01FFu * (uint32_t)(i * 2654435761u | 1u);
+    if (threadIdx.x == 0) {
+        mbar_init(&done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_base)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tb = tmem_base, sa = saddr(smem);
+    constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
+                               ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+    if (threadIdx.x == 0) {
+        // MN-major: 16-element groups along M (N) of 4 K-groups x 128 B; SBO = 512 B
+        const uint64_t ad = sdesc(sa, 128u, 512u), bd = sdesc(sa + ABYTES, 128u, 512u);
+        for (int64_t i = 0; i < iters; ++i) mma_i8(tb + (uint32_t)((i & 1) * 256), ad, bd, IDESC, i >= 2 ? 1u : 0u);
+        mma_commit(&done);
+        mbar_wait(&done, 0);
+    }
+    __syncwarp();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (threadIdx.x < 32) {
+        uint32_t v[16];
+        tmem_ld16(tb, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (v[0] == 0x12345678u) out[blockIdx.x] = v[1];
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512) : "memory");
+    }
+}
+
 }  // namespace hga
 
 extern "C" int hga_probe(int32_t kind, int64_t iters, int32_t blocks, int32_t threads, uint32_t* out,
                          void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (kind == 0)
+    if (kind == 0) {
         hga::k_probe_popc<<<blocks, threads, 0, st>>>(iters, 12345u, out);
-    else
+    } else if (kind == 1) {
         hga::k_probe_alu<<<blocks, threads, 0, st>>>(iters, 12345u, out);
+    } else if (kind == 2 || kind == 3) {
+        // one CTA per SM (116 KB of shared memory; the TMEM allocation is 512
+        // columns); `threads` ignored
+        const int smem = 116 * 1024;
+        auto k2 = hga::k_probe_mma_i8<128, 256>;
+        auto k3 = hga::k_probe_mma_i8<64, 64>;
+        cudaError_t e = cudaFuncSetAttribute(kind == 2 ? k2 : k3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return hga::to_rc(e);
+        if (kind == 2) k2<<<blocks, 128, smem, st>>>(iters, out);
+        else k3<<<blocks, 128, smem, st>>>(iters, out);
+    } else {
+        return HGA_E_INVALID;
+    }
     return hga::to_rc(cudaGetLastError());
 }

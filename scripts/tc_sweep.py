@@ -1,6 +1,8 @@
 """int8 fitness sweep at orders 36..64 on one path (for A/B of the fitness kernels).
 
-Usage: python scripts/tc_sweep.py TAG [PATH]   PATH = tc (HGA_FITNESS_TC=all) | popc (HGA_FITNESS_TC=0) | default
+Usage: python scripts/tc_sweep.py TAG [PATH]
+  PATH = tc2 (round-2 tcgen05 kernel, HGA_FITNESS_TC=2) | tc (round-1, HGA_FITNESS_TC=all)
+       | popc (XOR+POPC, HGA_FITNESS_TC=0) | default
 One JSON line per (m, variant): best of 10 CUDA-event timings after 3 warm-ups.
 """
 import json
@@ -11,7 +13,7 @@ from pathlib import Path
 tag = sys.argv[1] if len(sys.argv) > 1 else "run"
 path = sys.argv[2] if len(sys.argv) > 2 else "tc"
 if path != "default":
-    os.environ["HGA_FITNESS_TC"] = "all" if path == "tc" else "0"
+    os.environ["HGA_FITNESS_TC"] = {"tc": "all", "tc2": "2", "popc": "0"}[path]
 
 import torch  # noqa: E402
 
@@ -24,7 +26,8 @@ n = int(os.environ.get("NMAT", "1000000"))
 st = torch.cuda.current_stream().cuda_stream
 for m in orders:
     pop = engine.init_population_device(engine.GAConfig(order=m, population=n // 4, seed=2024))
-    for var, name in ((2, "f2"), (1, "f1"), (15, "all")):
+    for var, name in [(v, nm) for v, nm in ((2, "f2"), (1, "f1"), (8, "sq"), (15, "all"))
+                      if nm in os.environ.get("VARIANTS", "f2,f1,all").split(",")]:
         o = [torch.empty(n, dtype=torch.int64, device="cuda") if var & b else None for b in (1, 2, 4, 8)]
         ptrs = [x.data_ptr() if x is not None else None for x in o]
 
@@ -45,7 +48,7 @@ for m in orders:
             best = min(best, s.elapsed_time(e) / 1e3)
         byts = n * (m * m + 8 * bin(var).count("1"))
         print(json.dumps({"tag": tag, "path": path, "m": m, "n": n, "variant": name, "evals_per_s": n / best,
-                          "GBps": byts / best / 1e9, "frac_hbm": byts / best / 6532.5e9, "us": best * 1e6}),
+                          "GBps": byts / best / 1e9, "frac_hbm": byts / best / 6547.5e9, "us": best * 1e6}),
               flush=True)
     del pop
     torch.cuda.empty_cache()

@@ -95,31 +95,57 @@ def test_fitness_tensor_core_path_matches_popc_path(m, cuda_device, monkeypatch)
             pops.append(np.stack([h, -h, h.T]))
     for pop in pops:
         want = oracle.penalties(pop, threads=4)
-        monkeypatch.setenv("HGA_FITNESS_TC", "all")  # tensor cores at every order
+        monkeypatch.setenv("HGA_FITNESS_TC", "all")  # round-1 tensor-core kernel at every order
         got_tc = hga.penalties(pop)
         monkeypatch.setenv("HGA_FITNESS_TC", "0")
         got_pc = hga.penalties(pop)
+        monkeypatch.setenv("HGA_FITNESS_TC", "2")  # round-2 tensor-core kernel (orders 36..64)
+        got_t2 = hga.penalties(pop)
         monkeypatch.delenv("HGA_FITNESS_TC")
         for col, key in enumerate(("f1", "f2", "orth", "sq")):
             assert np.array_equal(got_tc[key], want[:, col]), (m, key, len(pop))
             assert np.array_equal(got_pc[key], want[:, col]), (m, key, len(pop))
+            assert np.array_equal(got_t2[key], want[:, col]), (m, key, len(pop), "tc2")
         for key in ("f1", "f2"):
             assert np.array_equal(hga.evaluate(pop, key), want[:, ("f1", "f2").index(key)])
 
 
 @pytest.mark.parametrize("m", list(range(4, 68, 4)))
-def test_fitness_tensor_core_rejects_non_sign(m, cuda_device, monkeypatch):
-    # the tensor-core path checks bytes in {-1, 0, +1} on the staged tiles and
-    # zeros through the Gram diagonal (g_jj = m): cover both halves
-    monkeypatch.setenv("HGA_FITNESS_TC", "all")
-    base = oracle.random_balanced(m, 5, 3, 1, 0, 0)
-    for (k, r, c, v) in ((0, 0, 0, 0), (4, m - 1, m - 1, 2), (2, m // 2, m - 1, -3), (3, 7 % m, 17 % m, 0),
-                         (1, 1 % m, 1 % m, -2), (0, m - 1, 0, -128), (4, 0, m // 2, 127)):
+@pytest.mark.parametrize("path", ["all", "2"])
+def test_fitness_tensor_core_rejects_non_sign(m, path, cuda_device, monkeypatch):
+    # round 1 checks bytes in {-1, 0, +1} on the staged tiles and zeros through
+    # the nonzero count; round 2 (orders 36..64) with the dp4a identity
+    # 128 sum v^2 == sum(127 v + u), sum v^2 == m^2: cover zeros, +-2, -3, the
+    # int8 extremes, and pairs that cancel in one sum but not the other
+    monkeypatch.setenv("HGA_FITNESS_TC", path)
+    base = oracle.random_balanced(m, 13, 3, 1, 0, 0)
+    cases = [[(0, 0, 0, 0)], [(4, m - 1, m - 1, 2)], [(2, m // 2, m - 1, -3)], [(3, 7 % m, 17 % m, 0)],
+             [(1, 1 % m, 1 % m, -2)], [(0, m - 1, 0, -128)], [(4, 0, m // 2, 127)], [(12, m - 1, m - 2, 0)],
+             [(9, 2, 3, 0), (9, 3, 3, 2)], [(8, 0, 1, 3), (8, 1, 1, -3)], [(7, m - 1, m - 1, -1 * 0)]]
+    for case in cases:
         pop = base.copy()
-        pop[k, r, c] = v
+        for (k, r, c, v) in case:
+            pop[k, r, c] = v
         with pytest.raises(ValueError):
             hga.evaluate(pop, "f2")
     assert np.array_equal(hga.evaluate(base, "f2"), oracle.evaluate(base, "f2"))
+
+
+@pytest.mark.parametrize("m", list(range(36, 68, 4)))
+def test_fitness_tc2_many_units_vs_oracle(m, cuda_device, monkeypatch):
+    """Round-2 tensor-core kernel over many pipeline units per CTA (stage and
+    TMEM-slot rings wrap many times, partial last unit), all four penalties
+    bit-exact; balanced and unbalanced populations."""
+    monkeypatch.setenv("HGA_FITNESS_TC", "2")
+    n = 148 * 8 * 9 + 5
+    pop = np.concatenate([oracle.random_balanced(m, n - 1000, 11 + m, 1, 0, 0),
+                          np.random.default_rng(m).choice(np.array([-1, 1], dtype=np.int8), size=(1000, m, m))])
+    want = oracle.penalties(pop)
+    got = hga.penalties(pop)
+    for col, key in enumerate(("f1", "f2", "orth", "sq")):
+        assert np.array_equal(got[key], want[:, col]), (m, key)
+    for key in ("f1", "f2", "sq"):
+        assert np.array_equal(hga.evaluate(pop, key), want[:, ("f1", "f2", "orth", "sq").index(key)]), (m, key)
 
 
 def test_fitness_large_population_sampled(cuda_device):
@@ -497,10 +523,13 @@ def test_single_gpu_island_and_elites(cuda_device):
     assert np.array_equal(fit_e.cpu().numpy(), fit[order])
     pop = isl.state.population
     assert np.array_equal(engine._unpack(rec_e.reshape(-1), 16, 20).cpu().numpy(), pop[order])
-    # migrants land in the first offspring slots and the loop keeps running
+    # migrants replace the 16 worst (largest fitness, lowest index first) and the loop keeps running
     isl.receive(rec_e, fit_e)
     after = isl.state.population
-    assert np.array_equal(after[1000:1016], pop[order])
+    worst = np.argsort(-fit, kind="stable")[:16]
+    slots = isl.last_received.cpu().numpy()
+    assert sorted(slots.tolist()) == sorted(worst.tolist())
+    assert np.array_equal(after[slots], pop[order])
     isl.advance(2)
     p2 = isl.state.population
     assert np.array_equal(isl.state.fitness, oracle.evaluate(p2, "f2"))

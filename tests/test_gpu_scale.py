@@ -114,7 +114,7 @@ def test_production_loop_at_measured_sizes(m, N, nc, nr, fit, sample, cuda_devic
 
 def test_production_loop_with_stall_restarts_at_bench_size(cuda_device):
     """Stall restarts (engine.py:518-525) at the bench population: a window of
-    1 forces a restart every generation the best does not improve; the
+    2 restarts whenever the best stays flat for two generations; the
     restart refills offspring from fresh Philox streams and the invariants
     and fitness must still hold."""
     cfg = engine.GAConfig(order=20, population=10_000, seed=77, fitness="f2", mutation_cols=4, mutation_row_pairs=2,
@@ -122,8 +122,9 @@ def test_production_loop_with_stall_restarts_at_bench_size(cuda_device):
     st = hga.initial_state(cfg)
     rng = np.random.default_rng(0)
     for _ in range(5):
-        engine._run_device(st, 12, force=True)
+        engine._run_device(st, 12)  # not forced: the device loop decides restarts itself
         _device_invariants(st, None, rng)
+        assert all(a >= b for a, b in zip(st.trace, st.trace[1:]))
     assert st._last_restart > 0, "no stall restart happened"
 
 
@@ -157,8 +158,10 @@ def test_host_step_non_ga_population_is_exact(m, N, fit, breakage, cuda_device):
     cfg = engine.GAConfig(order=m, population=N, seed=31, fitness=fit, mutation_cols=2, mutation_row_pairs=3)
     rng = np.random.default_rng(m)
     pop = oracle.init_population(m, N, 31)
+    # every matrix broken, so the breakage survives selection (columns move whole
+    # and mutation swaps keep column sums): all three steps take the exact path
     if breakage == "unbalanced":
-        pop[5, 0, 3] = -pop[5, 0, 3]
+        pop[:, 0, 3] = -pop[:, 0, 3]
     elif breakage == "first_column":
         pop[:, 1, 0] = -1
     else:
