@@ -8,10 +8,13 @@ calls that need it raise instead of computing anything on the host.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "libhga.so"
+if os.environ.get("HGA_LIB_VARIANT"):  # experiments: an A/B build next to the product library
+    LIB_PATH = HERE / f"libhga_{os.environ['HGA_LIB_VARIANT']}.so"
 
 # return codes / flags (include/hga.h)
 HGA_OK = 0
@@ -120,6 +123,8 @@ class _Lib:
                     "there is no CPU fallback")
             dll = ctypes.CDLL(str(LIB_PATH))
             for name, (res, args) in SIGNATURES.items():
+                if os.environ.get("HGA_LIB_VARIANT") and not hasattr(dll, name):
+                    continue  # fitness-only A/B build
                 fn = getattr(dll, name)
                 fn.restype = res
                 fn.argtypes = args

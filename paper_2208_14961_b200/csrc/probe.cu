@@ -44,18 +44,21 @@ __global__ void k_probe_alu(int64_t iters, uint32_t seed, uint32_t* out) {
 
 // Dense int8 tensor-core rate: one elected thread per CTA issues `iters`
 // back-to-back tcgen05.mma.kind::i8 (s8 x s8 -> s32) of shape M x N x 32 from
-// shared memory into two TMEM accumulators (MN-major no-swizzle operands, the
-// fitness kernels' layout), then waits for the last one.  ops = iters * 2MNK.
-// (M, N) = (128, 256): the largest single-CTA shape (the pipe's dense peak);
-// (64, 64): the fitness kernels' own shape (M = 64 runs half the datapath).
-template <int M, int N>
+// shared memory, MN-major no-swizzle operands (the fitness kernels' layout),
+// then waits for the last one.  ops = iters * 2MNK.  TILES = 1: the same
+// operand tile every time, two accumulators alternating (the pipe's best
+// case); TILES > 1: A = B = a different tile each instruction and
+// 512 / N accumulators in rotation (what the fitness kernels issue).
+template <int M, int N, int TILES>
 __global__ void __launch_bounds__(128, 1) k_probe_mma_i8(int64_t iters, uint32_t* out) {
     using namespace tcx;
-    extern __shared__ __align__(1024) uint8_t smem[];  // A: M x 32 bytes, B: N x 32 bytes
+    extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t done;
     __shared__ uint32_t tmem_base;
-    constexpr int ABYTES = M * 32, BBYTES = N * 32;
-    for (int i = threadIdx.x; i < (ABYTES + BBYTES) / 4; i += blockDim.x)
+    constexpr int MN = M > N ? M : N;
+    constexpr int TB = TILES == 1 ? (M + N) * 32 : MN * 32;  // bytes per tile
+    constexpr int NACC = TILES == 1 ? 2 : 512 / N;
+    for (int i = threadIdx.x; i < TILES * TB / 4; i += blockDim.x)
         reinterpret_cast<uint32_t*>(smem)[i] = 0x01FF01FFu * (uint32_t)(i * 2654435761u | 1u);
     if (threadIdx.x == 0) {
         mbar_init(&done, 1);
@@ -76,8 +79,12 @@ __global__ void __launch_bounds__(128, 1) k_probe_mma_i8(int64_t iters, uint32_t
                                ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
     if (threadIdx.x == 0) {
         // MN-major: 16-element groups along M (N) of 4 K-groups x 128 B; SBO = 512 B
-        const uint64_t ad = sdesc(sa, 128u, 512u), bd = sdesc(sa + ABYTES, 128u, 512u);
-        for (int64_t i = 0; i < iters; ++i) mma_i8(tb + (uint32_t)((i & 1) * 256), ad, bd, IDESC, i >= 2 ? 1u : 0u);
+        for (int64_t i = 0; i < iters; ++i) {
+            const uint32_t t = TILES == 1 ? 0u : (uint32_t)(i % TILES) * TB;
+            const uint64_t ad = sdesc(sa + t, 128u, 512u);
+            const uint64_t bd = TILES == 1 ? sdesc(sa + M * 32, 128u, 512u) : ad;
+            mma_i8(tb + (uint32_t)((i % NACC) * N), ad, bd, IDESC, i >= NACC ? 1u : 0u);
+        }
         mma_commit(&done);
         mbar_wait(&done, 0);
     }
@@ -103,16 +110,28 @@ extern "C" int hga_probe(int32_t kind, int64_t iters, int32_t blocks, int32_t th
         hga::k_probe_popc<<<blocks, threads, 0, st>>>(iters, 12345u, out);
     } else if (kind == 1) {
         hga::k_probe_alu<<<blocks, threads, 0, st>>>(iters, 12345u, out);
-    } else if (kind == 2 || kind == 3) {
+    } else if (kind >= 2 && kind <= 9) {
         // one CTA per SM (116 KB of shared memory; the TMEM allocation is 512
-        // columns); `threads` ignored
+        // columns); `threads` ignored.  2: 128x256 (same tile), 3: 64x64 (same
+        // tile), 4: 64x64 / 5: 64x48 / 6: 128x128 / 7: 128x96 / 8: 128x64 /
+        // 9: 128x256, each with a new 16-deep rotating tile per instruction
         const int smem = 116 * 1024;
-        auto k2 = hga::k_probe_mma_i8<128, 256>;
-        auto k3 = hga::k_probe_mma_i8<64, 64>;
-        cudaError_t e = cudaFuncSetAttribute(kind == 2 ? k2 : k3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        void* k = nullptr;
+        switch (kind) {
+            case 2: k = (void*)hga::k_probe_mma_i8<128, 256, 1>; break;
+            case 3: k = (void*)hga::k_probe_mma_i8<64, 64, 1>; break;
+            case 4: k = (void*)hga::k_probe_mma_i8<64, 64, 16>; break;
+            case 5: k = (void*)hga::k_probe_mma_i8<64, 48, 16>; break;
+            case 6: k = (void*)hga::k_probe_mma_i8<128, 128, 16>; break;
+            case 7: k = (void*)hga::k_probe_mma_i8<128, 96, 16>; break;
+            case 8: k = (void*)hga::k_probe_mma_i8<128, 64, 16>; break;
+            default: k = (void*)hga::k_probe_mma_i8<128, 256, 12>; break;
+        }
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return hga::to_rc(e);
-        if (kind == 2) k2<<<blocks, 128, smem, st>>>(iters, out);
-        else k3<<<blocks, 128, smem, st>>>(iters, out);
+        void* args[] = {(void*)&iters, (void*)&out};
+        e = cudaLaunchKernel(k, dim3(blocks), dim3(128), args, smem, st);
+        if (e != cudaSuccess) return hga::to_rc(e);
     } else {
         return HGA_E_INVALID;
     }

@@ -6,10 +6,10 @@ mkdir -p $out
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "tensor_core or tc2 or fuzz" > $out/tests.log 2>&1
 echo "tests_rc=$?" >> $out/tests.log
 tail -n 3 $out/tests.log
-for p in tc2 tc popc; do
+for p in ${PATHS:-tc2 tc popc}; do
   timeout 600 python scripts/tc_sweep.py $1 $p > $out/sweep_$p.jsonl 2> $out/sweep_$p.err
 done
-ORDERS=20,24,28,32 VARIANTS=f2 timeout 300 python scripts/tc_sweep.py $1 popc > $out/sweep_small.jsonl 2>&1
+[ -n "$SMALL" ] && ORDERS=20,24,28,32 VARIANTS=f2 timeout 300 python scripts/tc_sweep.py $1 popc > $out/sweep_small.jsonl 2>&1
 python - <<PY
 import json,glob
 rows=[json.loads(l) for f in sorted(glob.glob("$out/sweep_*.jsonl")) for l in open(f) if l.startswith("{")]

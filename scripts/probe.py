@@ -49,10 +49,13 @@ def probe_pipes():
         print(json.dumps({"probe": name, "ops_per_s": ops / t, "per_sm_per_clk_at_1965MHz": ops / t / sms / 1.965e9,
                           "sm_clock_mhz_now": clk}), flush=True)
     # dense int8 tcgen05.mma: kind 2 = 128x256x32 (pipe peak), kind 3 = 64x64x32 (the fitness kernels' shape)
-    for kind, (M, N), iters in ((2, (128, 256), 20000), (3, (64, 64), 200000)):
+    for kind, (M, N), iters, tag in ((2, (128, 256), 20000, "same_tile"), (3, (64, 64), 200000, "same_tile"),
+                                     (4, (64, 64), 200000, "rotating_tiles"), (5, (64, 48), 200000, "rotating_tiles"),
+                                     (6, (128, 128), 100000, "rotating_tiles"), (7, (128, 96), 100000, "rotating_tiles"),
+                                     (8, (128, 64), 100000, "rotating_tiles"), (9, (128, 256), 20000, "rotating_tiles")):
         t = timed(lambda: lib.hga_probe(kind, iters, sms, 128, out.data_ptr(), st), reps=5, warm=2)
         ops = sms * iters * 2 * M * N * 32
-        print(json.dumps({"probe": f"tcgen05_mma_i8_{M}x{N}x32", "ops_per_s": ops / t, "mma_per_s_per_sm": iters / t,
+        print(json.dumps({"probe": f"tcgen05_mma_i8_{M}x{N}x32_{tag}", "ops_per_s": ops / t, "mma_per_s_per_sm": iters / t,
                           "clk_per_mma_at_1965MHz": 1.965e9 * t / iters}), flush=True)
 
 

@@ -25,7 +25,11 @@ orders = [int(x) for x in os.environ.get("ORDERS", "36,40,44,48,52,56,60,64").sp
 n = int(os.environ.get("NMAT", "1000000"))
 st = torch.cuda.current_stream().cuda_stream
 for m in orders:
-    pop = engine.init_population_device(engine.GAConfig(order=m, population=n // 4, seed=2024))
+    if os.environ.get("HGA_LIB_VARIANT"):  # fitness-only A/B library: random +-1 input from torch
+        g = torch.Generator(device="cuda").manual_seed(2024 + m)
+        pop = (torch.randint(0, 2, (n, m, m), device="cuda", dtype=torch.int8, generator=g) * 2 - 1).contiguous()
+    else:
+        pop = engine.init_population_device(engine.GAConfig(order=m, population=n // 4, seed=2024))
     for var, name in [(v, nm) for v, nm in ((2, "f2"), (1, "f1"), (8, "sq"), (15, "all"))
                       if nm in os.environ.get("VARIANTS", "f2,f1,all").split(",")]:
         o = [torch.empty(n, dtype=torch.int64, device="cuda") if var & b else None for b in (1, 2, 4, 8)]
