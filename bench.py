@@ -117,6 +117,47 @@ class ClockSampler:
 # ---------------------------------------------------------------- our arm
 
 
+def load_peaks() -> dict:
+    """HBM from the driver-written MEASURED_PEAKS.json; the pipe ceilings
+    (POPC, int8 tcgen05) from the committed probe output profiles/r02_peaks.json
+    (scripts/probe.py --only pipes on this pool's B200)."""
+    peaks = {}
+    mp = ROOT / "MEASURED_PEAKS.json"
+    if mp.exists():
+        peaks.update({k: v for k, v in json.loads(mp.read_text()).items() if k in ("hbm_gbs", "bf16_tflops")})
+        peaks["hbm_source"] = "MEASURED_PEAKS.json hbm_gbs"
+    pp = ROOT / "profiles" / "r02_peaks.json"
+    if pp.exists():
+        d = json.loads(pp.read_text())
+        for k in ("popc_per_s", "alu_per_s", "int8_tc_dense_ops_per_s"):
+            if k in d:
+                peaks[k] = d[k]
+        for r in d.get("probes", []):
+            if r.get("probe", "").startswith("tcgen05_mma_i8_64x64x32_rotating"):
+                peaks["mma_64x64x32_per_s_per_sm"] = r["mma_per_s_per_sm"]
+        peaks["pipe_source"] = "profiles/r02_peaks.json (scripts/probe.py --only pipes)"
+    if "hbm_gbs" not in peaks:
+        peaks["hbm_gbs"], peaks["hbm_source"] = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    return peaks
+
+
+_NCU_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1024.0, "MB": 1024.0**2, "GB": 1024.0**3}
+
+
+def ncu_traffic(path: Path) -> float | None:
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch from a
+    committed ncu summary ({"metrics": {name: [unit, value]}})."""
+    try:
+        m = json.loads(path.read_text()).get("metrics", {})
+        tot = 0.0
+        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            unit, val = m[name]
+            tot += float(str(val).replace(",", "")) * _NCU_SCALE[unit]
+        return tot
+    except (OSError, ValueError, KeyError, TypeError):
+        return None
+
+
 def algorithmic_bytes_per_generation(m: int, n_pairs: int) -> int:
     """Minimum HBM traffic of one generation:
     read 4N fitness (selection), read the 2N selected parents, write the new
@@ -207,22 +248,21 @@ def run_ours(args, rank, world, local_rank):
 
     # roofline of the dominant (only) kernel of the step: k_run
     alg_bytes = algorithmic_bytes_per_generation(ORDER, N_PAIRS)
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peaks = load_peaks()
+    peak = float(peaks["hbm_gbs"])
     achieved = alg_bytes / per_step / 1e9
+    pairs = (ORDER - 1) * (ORDER - 2) // 2  # column 0 is all +1 in every GA individual
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "k_run (one generation, persistent cooperative kernel)",
-                "algorithmic_bytes_per_launch": alg_bytes,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
-                "popc_ceiling_evals_per_s": 4.52e12 / (ORDER * (ORDER - 1) // 2)}
-    prof = ROOT / "profiles" / "r01_k_run_traffic.json"
-    if prof.exists():
-        try:
-            t = json.loads(prof.read_text())
-            roofline["traffic"] = t.get("dram_bytes_per_launch",
-                                        (t.get("dram_bytes_read") or 0) + (t.get("dram_bytes_write") or 0) or None)
-        except (ValueError, OSError):
-            pass
+                "traffic": None, "kernel": "k_run_v3 (one generation, persistent cooperative kernel)",
+                "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peaks["hbm_source"],
+                "popc_frac": 2 * N_PAIRS * pairs / per_step / peaks["popc_per_s"] if "popc_per_s" in peaks else None,
+                "note": "latency-bound: a 40,000-matrix generation moves 5.4 MB and does 3.4M POPC "
+                        "(< 1 us of either ceiling); DESIGN.md section 3"}
+    for prof in (ROOT / "profiles" / "r02_k_run_traffic.json", ROOT / "profiles" / "r01_k_run_traffic.json"):
+        if prof.exists():
+            roofline["traffic"] = ncu_traffic(prof)
+            roofline["traffic_source"] = str(prof.relative_to(ROOT))
+            break
 
     # production mode: K generations back to back in ONE launch (no flush)
     a2 = res.run_args()
@@ -258,7 +298,9 @@ def run_ours(args, rank, world, local_rank):
                            "8-word state read back every step)"}
 
     # fitness-only sweep (config 5) at large n: the kernel's own roofline
-    sweep = run_fitness_sweep(args, engine, torch, lib, peak) if not args.no_sweep else None
+    sweep = run_fitness_sweep(args, engine, torch, lib, peaks) if not args.no_sweep else None
+    # the config-3 / config-4 island generation loops against their ceilings
+    gen_rows = run_generation_rows(args, engine, torch, lib, peaks) if not args.no_sweep else None
 
     out = {
         "metric": METRIC,
@@ -292,6 +334,8 @@ def run_ours(args, rank, world, local_rank):
     }
     if sweep:
         out["fitness_sweep"] = sweep
+    if gen_rows:
+        out["generation_rows"] = gen_rows
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args)
     if dist:
@@ -335,10 +379,13 @@ def run_e2e(args, cfg, hga, engine, torch):
                    "hadamard_ga.step; one hga_step_host call: H2D, pack, generation, chunked unpack + D2H)"}
 
 
-def run_fitness_sweep(args, engine, torch, lib, peak):
+def run_fitness_sweep(args, engine, torch, lib, peaks):
+    """hga_fitness_i8 (the drop-in evaluate) at config-5 sizes, F2, inputs
+    larger than L2; each row against its binding ceiling (committed peaks)."""
     sp = torch.cuda.current_stream().cuda_stream
+    peak = float(peaks["hbm_gbs"])
     rows = []
-    for m in (20, 28, 36, 48, 64):
+    for m in (20, 28, 36, 44, 48, 52, 56, 60, 64):
         n = 4_000_000 if m <= 28 else (2_000_000 if m <= 36 else 1_000_000)
         cfg = engine.GAConfig(order=m, population=n // 4, seed=7)
         pop = engine.init_population_device(cfg)
@@ -357,20 +404,70 @@ def run_fitness_sweep(args, engine, torch, lib, peak):
             ts.append(s.elapsed_time(e) / 1e3)
         t = statistics.median(ts)
         bytes_ = n * (m * m + 8)
-        popc_ceiling = 4.52e12 / ((m * (m - 1) // 2) * ((m + 31) // 32))
         hbm_ceiling = peak * 1e9 / (m * m + 8)
         ev = n / t
-        # orders >= 48 run the Gram on tcgen05 (kind::i8): the tensor work per
-        # matrix is far below the HBM time, so HBM is that path's ceiling
-        tc = 48 <= m <= 64
-        ceiling = hbm_ceiling if tc else min(popc_ceiling, hbm_ceiling)
-        rows.append({"m": m, "n": n, "path": "tcgen05 kind::i8" if tc else "XOR+POPC",
-                     "evals_per_s": ev, "GBps": bytes_ / t / 1e9, "hbm_frac": bytes_ / t / 1e9 / peak,
-                     "frac_of_binding_ceiling": ev / ceiling,
-                     "binding": "hbm" if (tc or hbm_ceiling < popc_ceiling) else "popc"})
+        # orders >= 44 run the Gram on tcgen05 (kind::i8, csrc/fitness_tc2.cu): HBM is that
+        # path's roofline; the XOR+POPC kernels are bound by min(HBM, POPC)
+        tc = 44 <= m <= 64
+        row = {"m": m, "n": n, "path": "tcgen05 kind::i8" if tc else "XOR+POPC", "evals_per_s": ev,
+               "GBps": bytes_ / t / 1e9, "hbm_frac": bytes_ / t / 1e9 / peak}
+        if tc:
+            row.update(binding="hbm", frac_of_binding_ceiling=ev / hbm_ceiling)
+            if "mma_64x64x32_per_s_per_sm" in peaks:  # two 64x64x32 MMAs per matrix (K = 64)
+                sms = torch.cuda.get_device_properties(0).multi_processor_count
+                row["tensor_issue_frac"] = 2 * ev / (peaks["mma_64x64x32_per_s_per_sm"] * sms)
+        else:
+            popc_ceiling = peaks.get("popc_per_s", float("inf")) / ((m * (m - 1) // 2) * ((m + 31) // 32))
+            binding = "hbm" if hbm_ceiling < popc_ceiling else "popc"
+            row.update(binding=binding, frac_of_binding_ceiling=ev / min(hbm_ceiling, popc_ceiling))
+        rows.append(row)
         del pop, out
         torch.cuda.empty_cache()
-    return {"kernel": "hga_fitness_i8 (int8 (n,m,m) drop-in layout, F2)", "inputs": "larger than L2", "rows": rows}
+    return {"kernel": "hga_fitness_i8 (int8 (n,m,m) drop-in layout, F2)", "inputs": "larger than L2",
+            "peaks": {k: v for k, v in peaks.items() if k != "probes"}, "rows": rows}
+
+
+def run_generation_rows(args, engine, torch, lib, peaks):
+    """The production loop at the config-3 / config-4 island sizes (BASELINE
+    configs[2] / [3] split over 8 GPUs): one persistent launch of K
+    generations after a warm-up launch, per-generation time, and its
+    fraction of the HBM and POPC ceilings (algorithmic bytes of section 4
+    of DESIGN.md; pair chain without column 0)."""
+    from paper_2208_14961_b200._lib import RUN_FORCE, check
+
+    sp = torch.cuda.current_stream().cuda_stream
+    rows = []
+    for tag, m, n_pairs, nc, nr, gens in (("C3 island (order 28, 1M / 8)", 28, 31_250, 1, 10, 200),
+                                          ("C4 island (order 36, 10M / 8)", 36, 312_500, 1, 12, 40)):
+        cfg = engine.GAConfig(order=m, population=n_pairs, seed=11, fitness="f2", mutation_cols=nc,
+                              mutation_row_pairs=nr, max_iterations=engine.MAX_ITERATIONS)
+        st = engine.initial_state(cfg)
+        res = st._res
+        res.ensure_trace(3 * gens + 8)
+        a = res.run_args()
+        a.gens_this_call = gens
+        a.flags = RUN_FORCE
+        check(lib.hga_run(a, sp), "hga_run")  # warm-up launch
+        torch.cuda.synchronize()
+        a = res.run_args()
+        a.gens_this_call = gens
+        a.flags = RUN_FORCE
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        check(lib.hga_run(a, sp), "hga_run")
+        e.record()
+        e.synchronize()
+        t = s.elapsed_time(e) / 1e3 / gens
+        alg = algorithmic_bytes_per_generation(m, n_pairs)
+        pairs = (m - 1) * (m - 2) // 2
+        popc = 2 * n_pairs * pairs * ((m + 31) // 32)
+        rows.append({"config": tag, "m": m, "matrices": 4 * n_pairs, "nc": nc, "nr": nr, "us_per_generation": t * 1e6,
+                     "offspring_evals_per_s": 2 * n_pairs / t, "algorithmic_bytes_per_generation": alg,
+                     "hbm_frac": alg / t / 1e9 / float(peaks["hbm_gbs"]),
+                     "popc_frac": popc / t / peaks["popc_per_s"] if "popc_per_s" in peaks else None})
+        del st, res
+        torch.cuda.empty_cache()
+    return rows
 
 
 # ---------------------------------------------------------------- cpu / reference arm
@@ -393,6 +490,22 @@ def cpu_baseline(args, budget_s: float = 12.0) -> dict:
                       f"oracle (oracle/hga_oracle.c, OpenMP fitness), {t:.1f} s"}
 
 
+def numpy_reference_timing() -> list | dict:
+    """The unmodified NumPy reference (hadamard_ga, installed under baseline/_ref
+    when present) timed on this host: evaluate() with 1 / all workers and
+    bench._timed_loop at the same workload (scripts/numpy_ref_timing.py).
+    Reported beside the C-port arm; the arm's value stays the C port."""
+    if not (ROOT / "baseline" / "_ref" / "hadamard_ga").exists():
+        return {"unavailable": "baseline/_ref not installed"}
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1")
+    try:
+        cp = subprocess.run([sys.executable, str(ROOT / "scripts" / "numpy_ref_timing.py"), "--gens", "3"], env=env,
+                            capture_output=True, text=True, timeout=240)
+        return [json.loads(ln) for ln in cp.stdout.splitlines() if ln.startswith("{")]
+    except (OSError, subprocess.TimeoutExpired, ValueError) as exc:
+        return {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return None
@@ -408,7 +521,9 @@ def run_reference(args, rank, world):
         oracle.step(st, threads)
     t = time.perf_counter() - t0
     value = 2 * N_PAIRS * steps / t
+    numpy_ref = numpy_reference_timing()
     return {
+        "numpy_reference": numpy_ref,
         "impl": "reference",
         "metric": METRIC,
         "value": value,

@@ -175,6 +175,16 @@ int hga_generation_explicit(uint32_t *pop, int64_t *fit, int64_t n_pairs, int32_
 int hga_argmin_key(const int64_t *fit, int64_t n, unsigned long long *key, int init,
                    void *stream);
 
+/* Device mirror of engine._check_state (engine.py:440-446, run when
+ * DEBUG_CHECKS is set): over n packed matrices counts[0] = matrices whose
+ * column 0 is not all +1, counts[1] = unbalanced columns (popcount != m/2),
+ * counts[2] = fitness values that differ from a fresh evaluation (variant
+ * fit_var).  ws: hga_check_invariants_ws_bytes(n) bytes. */
+size_t hga_check_invariants_ws_bytes(int64_t n);
+int hga_check_invariants(const uint32_t *cols, const int64_t *fit, int64_t n, int32_t m,
+                         uint32_t fit_var, unsigned long long *counts, void *ws, size_t ws_bytes,
+                         void *stream);
+
 /* ------------------------------------------------ production GA (Philox) */
 
 /* Arguments of the persistent, grid-synchronised generation loop. */

@@ -97,6 +97,8 @@ SIGNATURES = {
     "hga_compose_gather": (_int, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "hga_generation_explicit": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _i32, _i32, _u32, _vp, _vp]),
     "hga_argmin_key": (_int, [_vp, _i64, _vp, _int, _vp]),
+    "hga_check_invariants_ws_bytes": (_sz, [_i64]),
+    "hga_check_invariants": (_int, [_vp, _vp, _i64, _i32, _u32, _vp, _vp, _sz, _vp]),
     "hga_philox_init_packed": (_int, [_u64, _u64, _u64, _i64, _i64, _i32, _vp, _vp]),
     "hga_run_ws_bytes": (_sz, [_i64, _i32]),
     "hga_run_timing_offset": (_i64, [_i32]),

@@ -58,6 +58,9 @@ namespace tc2 {
 
 using namespace tcx;
 
+#ifndef HGA_TC2_M128
+#define HGA_TC2_M128 0
+#endif
 #ifndef HGA_TC2_FLAGS
 #define HGA_TC2_FLAGS 0
 #endif
@@ -86,7 +89,8 @@ constexpr int kMmaWarp = kProdWarp + 1;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
 constexpr int kSmemBytes = kCtasPerSm == 4 ? 52 * 1024 : (kCtasPerSm == 2 ? 108 * 1024 : 220 * 1024);
 constexpr int kTmemCols = 512 / kCtasPerSm;
-constexpr int kSlots = kTmemCols / (kB * 64) > 4 ? 4 : kTmemCols / (kB * 64);  // TMEM accumulator slots
+constexpr int kPairCols = HGA_TC2_M128 ? 128 : 64;  // TMEM columns per MMA pair
+constexpr int kSlots = kTmemCols / (kB * kPairCols) > 4 ? 4 : kTmemCols / (kB * kPairCols);  // accumulator slots
 constexpr int kBufs = kSlots + 1;     // finalisation ring depth (see header)
 constexpr int kMaxStages = 12;
 
@@ -97,8 +101,13 @@ struct Geo {
     // MMA N: 64 even at NCG = 3 -- measured (scripts/probe.py, rotating tiles) a
     // 64 x 48 x 32 MMA takes 92 clocks, 64 x 64 x 32 only 77; the extra Gram
     // columns 48..63 (B's fourth group = the next tile's first) are never read
-    static constexpr int N = 64;
-    static constexpr int TILE = NCG * 1024;          // tile pitch: NCG groups x 64 K-rows x 16 B
+    // M128 mode: one M = 128, N = 128 MMA per K step covers a PAIR -- A = B =
+    // the pair's two 4-group tiles back to back, the diagonal 64 x 64 blocks of
+    // D are the two Grams (same instruction time as 64 x 64, measured)
+    static constexpr bool M128 = HGA_TC2_M128 != 0;
+    static constexpr int N = M128 ? 128 : 64;
+    static constexpr int MM = M128 ? 128 : 64;       // MMA M
+    static constexpr int TILE = M128 ? 4096 : NCG * 1024;  // tile pitch: groups x 64 K-rows x 16 B
     static constexpr int RAW = M * M;                // raw matrix bytes (a multiple of 16)
     static constexpr int TSTAGE = kUnit * TILE;      // canonical tiles of one unit
     static constexpr int RSTAGE = (kUnit * RAW + 127) & ~127;  // raw bytes of one unit
@@ -107,7 +116,7 @@ struct Geo {
     static constexpr int RSTAGES = RS_FIT > kMaxStages ? kMaxStages : RS_FIT;
     static constexpr int SMEM = TSTAGES * TSTAGE + RSTAGES * RSTAGE + 1024;
     static constexpr int SLOT = kB * N;              // TMEM columns per slot
-    static constexpr int NQ = NCG == 3 ? 3 : 4;      // lane quarters holding real Gram rows
+    static constexpr int NQ = (M128 || NCG == 4) ? 4 : 3;  // lane quarters with Gram rows
     static constexpr int LASTW = (M - 16 * (NCG - 1)) / 4;  // valid 4-byte words of the last group
     static constexpr int MR = (M + 7) & ~7;          // rows per group in the relayout walk
     static constexpr int CHUNKS = NCG * MR;          // relayout slots per matrix
@@ -115,7 +124,7 @@ struct Geo {
     static constexpr uint32_t IDESC = (2u << 4)                    // D: s32
                                       | (1u << 7) | (1u << 10)     // A, B: signed 8-bit
                                       | (1u << 15) | (1u << 16)    // A, B: MN-major
-                                      | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(64 >> 4) << 24);
+                                      | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(MM >> 4) << 24);
     static_assert(kSlots >= 2 && kSlots * SLOT <= kTmemCols, "at least two TMEM slots");
     static_assert(RSTAGES >= 2, "at least two raw stages");
 };
@@ -134,6 +143,37 @@ __device__ __forceinline__ void check_word(uint32_t x, int& sq, int& lin) {
 }
 
 // Row sums of quarter Q over its Gram blocks (q, q + d mod NCG), d = 0..NB-1.
+// M128 layout: lane = Gram row; HALF 0 = rows 0..31 (row blocks 0, 1), HALF 1 =
+// rows 32..63.  HALF 0 reads column blocks 0, 1 (weight 1: both diagonal blocks
+// and the {0,1} pair from both sides) and 2 .. NCG-1 (weight 2); HALF 1 reads
+// column blocks 2 .. NCG-1 with weight 1 (rows >= m are zero).
+template <int M, int VM, int HALF>
+__device__ __forceinline__ void half_sums(uint32_t taddr, uint32_t& s1, uint32_t& s2, uint32_t& s4) {
+    using G = Geo<M>;
+    constexpr int C0 = HALF == 0 ? 0 : 2;
+    constexpr int NB = G::NCG - C0;
+    uint32_t v[NB][16];
+#pragma unroll
+    for (int d = 0; d < NB; ++d) tmem_ld16(taddr + (uint32_t)(16 * (C0 + d)), v[d]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    s1 = s2 = s4 = 0;
+#pragma unroll
+    for (int d = 0; d < NB; ++d) {
+        uint32_t a = 0, z = 0, q = 0;
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+            const int g0 = (int)v[d][e], g1 = (int)v[d][e + 1];
+            if constexpr ((VM & HGA_VAR_F1) != 0) a += (uint32_t)abs(g0) + (uint32_t)abs(g1);
+            if constexpr ((VM & (HGA_VAR_F2 | HGA_VAR_ORTH)) != 0) z = add_nonzero(add_nonzero(z, (uint32_t)g0), (uint32_t)g1);
+            if constexpr ((VM & HGA_VAR_SQ) != 0) q += (uint32_t)(g0 * g0) + (uint32_t)(g1 * g1);
+        }
+        const uint32_t w = (HALF == 0 && C0 + d >= 2) ? 2u : 1u;
+        s1 += w * a;
+        s2 += w * z;
+        s4 += w * q;
+    }
+}
+
 template <int M, int VM, int Q>
 __device__ __forceinline__ void quarter_sums(uint32_t taddr, uint32_t& s1, uint32_t& s2, uint32_t& s4) {
     using G = Geo<M>;
@@ -236,6 +276,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
                 const uint32_t st = sbase + (uint32_t)(ts * G::TSTAGE);
+                if constexpr (G::M128) {
+                    // pair b: tiles 2b, 2b+1 back to back = one 128-row operand; D columns b * 128
+#pragma unroll
+                    for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+                        for (int b = 0; b < kB; ++b) {
+                            const uint64_t desc = sdesc(st + (uint32_t)(2 * b * G::TILE + ks * 512), 128u, 1024u);
+                            if constexpr (!(flags & 2))
+                                mma_i8(tbase + (uint32_t)(a * G::SLOT + b * 128), desc, desc, G::IDESC, ks > 0 ? 1u : 0u);
+                        }
+                } else {
                 // K step 0 of every tile, then K step 1: consecutive MMAs never feed the
                 // same accumulator (a dependent pair would wait for the first's result)
 #pragma unroll
@@ -248,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                         const uint64_t desc = sdesc(tile + (uint32_t)(ks * 512), 128u, 1024u);
                         if constexpr (!(flags & 2)) mma_i8(d, desc, desc, G::IDESC, ks > 0 ? 1u : 0u);
                     }
+                }
                 }
                 mma_commit(&tfree[ts]);
                 mma_commit(&tfull[a]);
@@ -346,18 +398,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 const int a = it % kSlots, buf = it % kBufs;
                 mbar_wait(&tfull[a], (it / kSlots) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t taddr = tbase + (uint32_t)(a * G::SLOT + g * G::N) + ((uint32_t)(32 * q) << 16);
+                const uint32_t taddr = G::M128
+                                           ? tbase + (uint32_t)(a * G::SLOT + g * 128 + 64 * (q >> 1)) + ((uint32_t)(32 * q) << 16)
+                                           : tbase + (uint32_t)(a * G::SLOT + g * G::N) + ((uint32_t)(32 * q) << 16);
                 uint32_t s1 = 0, s2 = 0, s4 = 0;
                 if constexpr ((flags & 4) != 0) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[a]);
                     continue;
                 }
-                switch (q) {
-                    case 0: quarter_sums<M, VM, 0>(taddr, s1, s2, s4); break;
-                    case 1: quarter_sums<M, VM, 1>(taddr, s1, s2, s4); break;
-                    case 2: quarter_sums<M, VM, 2>(taddr, s1, s2, s4); break;
-                    default: quarter_sums<M, VM, 3>(taddr, s1, s2, s4); break;
+                if constexpr (G::M128) {
+                    if (q & 1) half_sums<M, VM, 1>(taddr, s1, s2, s4);
+                    else half_sums<M, VM, 0>(taddr, s1, s2, s4);
+                } else {
+                    switch (q) {
+                        case 0: quarter_sums<M, VM, 0>(taddr, s1, s2, s4); break;
+                        case 1: quarter_sums<M, VM, 1>(taddr, s1, s2, s4); break;
+                        case 2: quarter_sums<M, VM, 2>(taddr, s1, s2, s4); break;
+                        default: quarter_sums<M, VM, 3>(taddr, s1, s2, s4); break;
+                    }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
@@ -366,7 +425,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 uint32_t p[2][3] = {{0u, 0u, 0u}, {0u, 0u, 0u}};
 #pragma unroll
                 for (int jj = 0; jj < 2; ++jj) {
-                    const bool mine = j == jj;
+                    // M128: the whole warp is one matrix (q / 2); else lanes 16-31 are matrix 1
+                    const bool mine = G::M128 ? (q >> 1) == jj : j == jj;
                     if constexpr ((VM & HGA_VAR_F1) != 0) p[jj][0] = __reduce_add_sync(0xffffffffu, mine ? s1 : 0u);
                     if constexpr ((VM & (HGA_VAR_F2 | HGA_VAR_ORTH)) != 0)
                         p[jj][1] = __reduce_add_sync(0xffffffffu, mine ? s2 : 0u);

@@ -234,6 +234,32 @@ __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v;
 
 using namespace hga;
 
+// _check_state (engine.py:440-446) on the packed resident population: per
+// (matrix, column) thread, column 0 must have no -1 bit and every other
+// column exactly m/2; per matrix (column-0 thread) the stored fitness must
+// equal the freshly recomputed one.  counts[0] = bad first columns,
+// counts[1] = unbalanced columns, counts[2] = stale fitness values.
+__global__ void k_check_invariants(const uint32_t* __restrict__ cols, const int64_t* __restrict__ fit,
+                                   const int64_t* __restrict__ fresh, int64_t n, int m,
+                                   unsigned long long* counts) {
+    const int W = words_for(m);
+    unsigned long long c0 = 0, c1 = 0, c2 = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * m; t += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(t % m);
+        int neg = 0;
+        for (int w = 0; w < W; ++w) neg += __popc(cols[t * W + w]);
+        if (j == 0) {
+            c0 += neg != 0;
+            c2 += fit[t / m] != fresh[t / m];
+        } else {
+            c1 += neg != m / 2;
+        }
+    }
+    if (c0) atomicAdd(&counts[0], c0);
+    if (c1) atomicAdd(&counts[1], c1);
+    if (c2) atomicAdd(&counts[2], c2);
+}
+
 extern "C" {
 
 int hga_crossover_i8(int8_t* pop, int64_t total, int32_t m, const int64_t* points, int32_t* bad_flag,
@@ -310,6 +336,27 @@ int hga_compose_gather(const int64_t* order, const int64_t* perm, int64_t count,
         k_compose_gather<uint8_t><<<grid_1d(count * bytes_per_matrix), 256, 0, st>>>(
             order, perm, count, (const uint8_t*)src, (uint8_t*)dst, bytes_per_matrix, fit_src, fit_dst, chosen);
     }
+    return to_rc(cudaGetLastError());
+}
+
+size_t hga_check_invariants_ws_bytes(int64_t n) { return n > 0 ? (size_t)n * sizeof(int64_t) : 0; }
+
+int hga_check_invariants(const uint32_t* cols, const int64_t* fit, int64_t n, int32_t m, uint32_t fit_var,
+                         unsigned long long* counts, void* ws, size_t ws_bytes, void* stream) {
+    if (n < 0 || m < 4 || m > 4096 || (m & 3) || !counts ||
+        (fit_var != HGA_VAR_F1 && fit_var != HGA_VAR_F2 && fit_var != HGA_VAR_SQ))
+        return HGA_E_INVALID;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(counts, 0, 3 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return to_rc(e);
+    if (n == 0) return HGA_OK;
+    if (!ws || ws_bytes < hga_check_invariants_ws_bytes(n)) return HGA_E_WORKSPACE;
+    int64_t* fresh = (int64_t*)ws;
+    const int rc = hga_fitness_packed(cols, n, m, fit_var, fit_var == HGA_VAR_F1 ? fresh : nullptr,
+                                      fit_var == HGA_VAR_F2 ? fresh : nullptr, nullptr,
+                                      fit_var == HGA_VAR_SQ ? fresh : nullptr, stream);
+    if (rc) return rc;
+    k_check_invariants<<<grid_1d(n * (int64_t)m), 256, 0, st>>>(cols, fit, fresh, n, m, counts);
     return to_rc(cudaGetLastError());
 }
 

@@ -922,11 +922,27 @@ def _finish_host_step(state, pop_np: np.ndarray, fit_np: np.ndarray, it1: int, f
         state.best_matrix = pop_np[int(np.argmin(fit_np))].copy()
 
 
+def check_invariants(state: SearchState) -> tuple[int, int, int]:
+    """(bad first columns, unbalanced columns, stale fitness values) of the
+    device-resident population, counted on the GPU (hga_check_invariants)."""
+    res = state._res
+    total = 4 * res.N
+    counts = torch.zeros(3, dtype=torch.int64, device=res.dev)
+    wsb = int(lib.hga_check_invariants_ws_bytes(total))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=res.dev)
+    check(lib.hga_check_invariants(res.pop[res.cur].data_ptr(), res.fit[res.cur].data_ptr(), total, res.m,
+                                   res.fit_var, counts.data_ptr(), ws.data_ptr(), wsb, stream_ptr()),
+          "hga_check_invariants")
+    c = counts.tolist()
+    return int(c[0]), int(c[1]), int(c[2])
+
+
 def _check_state(state: SearchState) -> None:
-    pop = state.population
-    assert (pop[:, :, 0] == 1).all(), "first column lost its all-+1 contract"
-    assert (pop[:, :, 1:].sum(axis=1, dtype=np.int64) == 0).all(), "column balance broken"
-    assert np.array_equal(state.fitness, evaluate(pop, state.config.fitness)), "fitness vector is stale"
+    """engine.py:440-446, on the device (no host copy of the population)."""
+    c0, c1, c2 = check_invariants(state)
+    assert c0 == 0, "first column lost its all-+1 contract"
+    assert c1 == 0, "column balance broken"
+    assert c2 == 0, "fitness vector is stale"
 
 
 def detect_stall(state: SearchState, window: int) -> bool:

@@ -88,7 +88,7 @@ if (src / "k_run.ncu-rep").exists():
               open(dst / f"{pre}_k_run_traffic.json", "w"), indent=1)
 
 # fitness sweep -> CSV
-popc = 4.52e12
+popc = json.loads((Path(__file__).resolve().parents[1] / "profiles" / "r02_peaks.json").read_text())["popc_per_s"]
 with open(dst / f"{pre}_fitness_sweep.csv", "w") as f:
     f.write("m,n,kernel,path,variant,evals_per_s,GBps,hbm_ceiling_evals,popc_ceiling_evals,frac_of_hbm\n")
     for line in open(src / "fitness_sweep.jsonl"):

@@ -330,3 +330,30 @@ def test_two_gpu_islands_on_one_device(cuda_device):
         assert (q_.T @ q_ == 20 * np.eye(20, dtype=np.int64)).all()
     else:
         assert migrations >= 1 and iters == 400
+
+
+# ------------------------------------------------------------ device invariant check (engine.py:440-446)
+
+
+def test_device_invariant_check_counts_violations(cuda_device, monkeypatch):
+    cfg = engine.GAConfig(order=28, population=2000, seed=3, fitness="f1", mutation_cols=2, mutation_row_pairs=3)
+    st = hga.initial_state(cfg)
+    engine._run_device(st, 5)
+    assert engine.check_invariants(st) == (0, 0, 0)
+    monkeypatch.setattr(engine, "DEBUG_CHECKS", True)
+    hga.step(st)  # runs _check_state on the device after the generation
+    res = st._res
+    pop = res.pop[res.cur].view(cfg.total, cfg.order, res.W)
+    saved = pop.clone()
+    fsaved = res.fit[res.cur].clone()
+    pop[7, 0, 0] ^= 1          # column 0 of matrix 7 gets a -1 (and becomes unbalanced-looking: counted once as c0)
+    pop[9, 5, 0] ^= 0b11       # column 5 of matrix 9: popcount m/2 -> m/2 +- 2 (or unchanged when the bits differ)
+    pop[11, 3, 0] ^= 1         # column 3 of matrix 11: popcount changes by one
+    res.fit[res.cur][13] += 8  # stale fitness
+    c0, c1, c2 = engine.check_invariants(st)
+    assert c0 == 1 and c1 >= 1 and c2 >= 1  # the corrupted matrices' recomputed fitness also differs
+    with pytest.raises(AssertionError):
+        engine._check_state(st)
+    pop.copy_(saved)
+    res.fit[res.cur].copy_(fsaved)
+    assert engine.check_invariants(st) == (0, 0, 0)
