@@ -142,6 +142,12 @@ int hga_mutate_i8(int8_t *pop, int64_t total, int32_t m, const int64_t *cols,
  * Fitness values may be any int64 whose range (max - min) is below
  * hga_select_max_range(); otherwise HGA_FLAG_FIT_RANGE is raised. */
 int64_t hga_select_max_range(void);
+/* Any-range variant (stable radix sort of all `total` (fitness, index)
+ * pairs; any int64 values): the first k indices of the stable argsort.
+ * Used when the histogram path raised HGA_FLAG_FIT_RANGE.  total < 2^31. */
+size_t hga_select_radix_ws_bytes(int64_t total);
+int hga_select_smallest_radix(const int64_t *fitness, int64_t total, int64_t k, int64_t *order,
+                              void *ws, size_t ws_bytes, void *stream);
 size_t hga_select_ws_bytes(int64_t total);
 int hga_select_order(const int64_t *fitness, int64_t total, int64_t *order, int32_t *bad_flag,
                      void *ws, size_t ws_bytes, void *stream);

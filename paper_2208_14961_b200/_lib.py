@@ -92,6 +92,8 @@ SIGNATURES = {
     "hga_mutate_i8": (_int, [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
     "hga_select_max_range": (_i64, []),
     "hga_select_ws_bytes": (_sz, [_i64]),
+    "hga_select_radix_ws_bytes": (_sz, [_i64]),
+    "hga_select_smallest_radix": (_int, [_vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "hga_select_order": (_int, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "hga_select_smallest": (_int, [_vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "hga_compose_gather": (_int, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),

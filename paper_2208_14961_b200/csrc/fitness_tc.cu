@@ -450,11 +450,12 @@ static int launch_tc(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int6
                      int32_t* bad, cudaStream_t st) {
     auto kern = k_fit_i8_tc<M, VM, OW>;
     constexpr int smem = Geo<M>::STAGES * 2 * kB * Geo<M>::TILE;
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return to_rc(e);
-        attr = true;
+        attr[dev] = true;
     }
     const int64_t nunits = (n + kB * Geo<M>::MPP - 1) / (kB * Geo<M>::MPP);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nunits, sm_count_cached()));

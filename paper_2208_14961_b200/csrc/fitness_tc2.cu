@@ -488,13 +488,12 @@ static int launch(const int8_t* pop, int64_t n, uint32_t v, int64_t* f1, int64_t
                   int32_t* bad, cudaStream_t st) {
     using G = Geo<M>;
     auto kern = k_fit_i8_tc2<M, VM>;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    static bool attr[64] = {};  // per device: the attribute is a property of the device's module
-    if (dev < 0 || dev >= 64 || !attr[dev]) {
+    static bool attr[kMaxDevices] = {};  // per device: the attribute is a property of the device's module
+    const int dev = current_device();
+    if (!attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
         if (e != cudaSuccess) return to_rc(e);
-        if (dev >= 0 && dev < 64) attr[dev] = true;
+        attr[dev] = true;
     }
     const int64_t nunits = (n + kUnit - 1) / kUnit;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nunits, (int64_t)kCtasPerSm * sm_count_cached()));

@@ -139,6 +139,16 @@ __device__ __forceinline__ int pair_steps(int m, int i) {
 
 int sm_count_cached();
 
+// Launch setup that is a property of the device (function attributes,
+// occupancy) is cached per device index: a process that drives several GPUs
+// sets it up on each of them.  Concurrent first calls write identical values.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return (d >= 0 && d < kMaxDevices) ? d : 0;
+}
+
 inline int to_rc(cudaError_t e) { return e == cudaSuccess ? HGA_OK : (int)HGA_E_CUDA_BASE + (int)e; }
 
 }  // namespace hga

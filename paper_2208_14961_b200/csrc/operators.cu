@@ -6,6 +6,8 @@
 //   select_order   argsort(F, stable)[:total/2]             (engine.py:245)
 //   compose_gather chosen = order[perm]; rows/fitness gather (engine.py:246-248)
 //   argmin_key     first-minimum argmin                      (engine.py:417, 432)
+#include <cub/device/device_radix_sort.cuh>
+
 #include "hga_common.cuh"
 
 namespace hga {
@@ -198,6 +200,24 @@ __global__ void __launch_bounds__(1024) k_sel_scatter(const int64_t* __restrict_
     }
 }
 
+// Any-range fallback: stable LSD radix sort of (fitness, index) pairs.  int64
+// keys become order-preserving uint64 (sign bit flipped); CUB's radix sort is
+// stable, so equal values keep index order (the stable-argsort tie rule).
+__global__ void k_sel_radix_prep(const int64_t* __restrict__ f, int64_t n, unsigned long long* __restrict__ keys,
+                                 int64_t* __restrict__ idx) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = (unsigned long long)f[i] ^ 0x8000000000000000ull;
+        idx[i] = i;
+    }
+}
+
+static size_t radix_temp_bytes(int64_t n) {
+    size_t t = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (int64_t*)nullptr, (int64_t*)nullptr, (int)n);
+    return (t + 255) & ~(size_t)255;
+}
+
 // -------------------------------------------------------- compose + gather
 template <typename V>
 __global__ void k_compose_gather(const int64_t* __restrict__ order, const int64_t* __restrict__ perm,
@@ -291,6 +311,30 @@ int hga_select_order(const int64_t* fitness, int64_t total, int64_t* order, int3
                      size_t ws_bytes, void* stream) {
     if (total < 0) return HGA_E_INVALID;
     return hga_select_smallest(fitness, total, total / 2, order, bad_flag, ws, ws_bytes, stream);
+}
+
+size_t hga_select_radix_ws_bytes(int64_t total) {
+    if (total <= 0 || total >= ((int64_t)1 << 31)) return 0;
+    return (size_t)total * 32 + radix_temp_bytes(total);
+}
+
+int hga_select_smallest_radix(const int64_t* fitness, int64_t total, int64_t k, int64_t* order, void* ws,
+                              size_t ws_bytes, void* stream) {
+    if (total < 0 || total >= ((int64_t)1 << 31) || k < 0 || k > total) return HGA_E_INVALID;
+    if (k == 0) return HGA_OK;
+    if (!ws || ws_bytes < hga_select_radix_ws_bytes(total)) return HGA_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* keys_in = (unsigned long long*)ws;
+    unsigned long long* keys_out = keys_in + total;
+    int64_t* idx_in = (int64_t*)(keys_out + total);
+    int64_t* idx_out = idx_in + total;
+    void* temp = idx_out + total;
+    size_t temp_bytes = radix_temp_bytes(total);
+    k_sel_radix_prep<<<grid_1d(total), 256, 0, st>>>(fitness, total, keys_in, idx_in);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, idx_in, idx_out, (int)total,
+                                                    0, 64, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(order, idx_out, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+    return to_rc(e);
 }
 
 int hga_select_smallest(const int64_t* fitness, int64_t total, int64_t k, int64_t* order, int32_t* bad_flag,

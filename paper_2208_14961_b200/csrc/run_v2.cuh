@@ -51,7 +51,7 @@ struct RunWs2 {
     uint32_t kmax[3];
     uint32_t cnt_lt[kR2MaxGrid];
     uint32_t cnt_eq[kR2MaxGrid];
-    uint32_t hist[3][kR2Bins];
+    alignas(16) uint32_t hist[3][kR2Bins];  // 16-byte aligned: bulk-prefetched into L2 at launch
     unsigned long long tstamp[64][20];  // HGA_RUN_TIMING: %globaltimer at phase boundaries (CTA 0)
     // followed by lt_list[4N], eq_list[4N] (uint64 (F << 32) | index): each CTA's survivors, compacted in index
     // order (two-barrier loop), then keys[2][run2_key_stride] (uint16 F >> granule per slot, padded with 0xFFFF;
@@ -966,6 +966,27 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
 
     int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
     int parity = (int)A.state[3];
+    {
+        // Cold launches (one generation per launch, L2 flushed by whatever ran before):
+        // bulk-prefetch the current population, its fitness and the select histogram
+        // into L2 at once, spread over all CTAs, so the dependent reads of the first
+        // generation hit L2 instead of paying an HBM round trip each.
+        const int64_t pieces[3] = {total * (int64_t)G::MW * 4, total * 8, (int64_t)kR2Bins * 4};
+        const char* bases[3] = {reinterpret_cast<const char*>(A.pop[parity]),
+                                reinterpret_cast<const char*>(A.fit[parity]),
+                                reinterpret_cast<const char*>(&ws->hist[ONE ? (int)((iter + 1) % 3) : (int)((iter + 1) & 1)][0])};
+        constexpr int64_t kPiece = 4096;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const int64_t np = (pieces[r] + kPiece - 1) / kPiece;
+            for (int64_t pc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pc < np; pc += (int64_t)gridDim.x * blockDim.x) {
+                const int64_t off = pc * kPiece;
+                const uint32_t len = (uint32_t)min(kPiece, pieces[r] - off) & ~15u;
+                if (len)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(bases[r] + off), "r"(len) : "memory");
+            }
+        }
+    }
     int64_t run = A.state[6], last_val = A.state[7];
     const bool force = (A.flags & HGA_RUN_FORCE) != 0;
     bool stop = !force && A.state[5] != 0;
@@ -1381,17 +1402,21 @@ int launch_run_v2_k(const hga_run_args* a, cudaStream_t st) {
     P.gshift = run2_granule_shift(a->fit_var);
     const int smem = GROUPS * (int)run_group_bytes<M, TP>();
     auto kern = k_run_v3<M, VM, GROUPS, ONE, TP>;
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[kMaxDevices] = {};
+    static int per_sm_dev[kMaxDevices] = {};  // 0 = not yet queried on that device
+    const int dev = current_device();
+    if (!attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return to_rc(e);
-        attr = true;
+        attr[dev] = true;
     }
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kR2Threads * GROUPS, smem);
+    if (per_sm_dev[dev] == 0) {
+        int v = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, kR2Threads * GROUPS, smem);
         if (e != cudaSuccess) return to_rc(e);
+        per_sm_dev[dev] = v > 0 ? v : -1;
     }
+    const int per_sm = per_sm_dev[dev];
     if (per_sm < 1) return HGA_E_UNSUPPORTED;
     const int grid = std::min(std::min(sm_count_cached() * std::min(per_sm, 2), kMaxNb), GROUPS * kR2Threads);
     void* params[] = {&P};

@@ -312,7 +312,8 @@ def select(population, fitness_values, stream) -> None:
     flag = _dev.new_flag()
     check(lib.hga_select_order(fit.data_ptr(), total, order.data_ptr(), flag.data_ptr(), ws.data_ptr(), wsb,
                                stream_ptr()), "hga_select_order")
-    _check_flag(flag, "select")
+    if int(flag.item()) & FLAG_FIT_RANGE:  # values span more than the histogram: stable radix sort
+        _select_radix(fit, total, half, order)
     seed, sid, counter = int(stream.seed), int(stream.stream_id), int(stream.counter)
     perm = torch.empty(half, dtype=torch.int64, device=dev)
     pwsb = int(lib.hga_ref_permutation_ws_bytes(half))
@@ -331,6 +332,19 @@ def select(population, fitness_values, stream) -> None:
         _copy_back(population, pop)
     if host_fit:
         _copy_back(fitness_values, fit)
+
+
+def _select_radix(fit: torch.Tensor, total: int, k: int, order: torch.Tensor) -> None:
+    """order[:k] = the first k indices of the stable argsort of fit (any int64 values)."""
+    wsb = int(lib.hga_select_radix_ws_bytes(total))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=fit.device)
+    check(lib.hga_select_smallest_radix(fit.data_ptr(), total, k, order.data_ptr(), ws.data_ptr(), wsb, stream_ptr()),
+          "hga_select_smallest_radix")
+
+
+def _fitness_bound(m: int, fit_var: int) -> int:
+    """Largest value the GA fitness variant can take at order m."""
+    return {1: m * m * (m - 1), 2: m * (m - 1), 8: m ** 3 * (m - 1)}[fit_var]
 
 
 def draw_crossover_points(config: GAConfig, seed: int, generation: int) -> np.ndarray:
@@ -534,17 +548,20 @@ class SearchState:
 
     @property
     def population(self) -> np.ndarray:
-        r = self._res
-        return _unpack(r.pop[r.cur], 4 * r.N, r.m).cpu().numpy()
+        return self.population_device.cpu().numpy()
 
     @property
     def population_device(self) -> torch.Tensor:
         r = self._res
+        if isinstance(r, _ResidentI8):
+            return r.pop[r.cur]
         return _unpack(r.pop[r.cur], 4 * r.N, r.m)
 
     @property
     def packed_population(self) -> torch.Tensor:
         r = self._res
+        if isinstance(r, _ResidentI8):
+            return _pack(r.pop[r.cur]).view(4 * r.N, r.m, r.W)
         return r.pop[r.cur].view(4 * r.N, r.m, r.W)
 
     @property
@@ -568,7 +585,7 @@ def initial_state(config: GAConfig, seed: int | None = None, workers: int = 1) -
         seed = config.seed if config.seed is not None else random_seed()
     seed &= MASK64
     if config.order > MAX_RESIDENT_ORDER:
-        raise HgaError(f"resident GA supports order <= {MAX_RESIDENT_ORDER}")
+        return _initial_state_i8(config, seed)
     res = _Resident(config, seed)
     m, total = config.order, config.total
     if config.rng == "reference":
@@ -589,6 +606,116 @@ def initial_state(config: GAConfig, seed: int | None = None, workers: int = 1) -
     return SearchState(config, seed, res, 0, int(best), [int(best)], _best_from_packed(res, res.best_packed))
 
 
+class _ResidentI8:
+    """Device side of a SearchState at orders above MAX_RESIDENT_ORDER (up to the
+    reference's 4096, engine.py:57): the reference's own int8 (4N, m, m)
+    layout in ping-pong buffers, advanced by the explicit-plan operator
+    kernels (select / permutation / gather, crossover_i8, mutate_i8,
+    fitness_i8) with the reference's counter streams, so a seeded run is the
+    reference's run.  (Orders <= 128 use the packed resident loops.)"""
+
+    def __init__(self, config: GAConfig, seed: int):
+        self.config = config
+        self.seed = seed
+        self.dev = _dev.require_cuda()
+        m, N = config.order, config.population
+        self.m, self.N, self.W = m, N, words_for(m)
+        total = 4 * N
+        self.pop = [torch.empty((total, m, m), dtype=torch.int8, device=self.dev) for _ in range(2)]
+        self.fit = [torch.empty(total, dtype=torch.int64, device=self.dev) for _ in range(2)]
+        self.cur = 0
+        self.fit_var = VARIANT_BITS[config.fitness]
+        self.key = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        wsb = int(lib.hga_fitness_i8_ws_bytes(total, m))
+        self.fws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=self.dev)
+        self.sel_ws = torch.empty(int(lib.hga_select_ws_bytes(total)), dtype=torch.uint8, device=self.dev)
+        pwsb = int(lib.hga_ref_permutation_ws_bytes(2 * N))
+        self.perm_ws = torch.empty(max(pwsb, 1), dtype=torch.uint8, device=self.dev)
+
+    argmin = _Resident.argmin
+
+    def init_slots(self, buf: int, purpose: int, generation: int, first: int, count: int) -> None:
+        """Reference-stream balanced matrices (engine.py:154-182) into slots [first, first+count)."""
+        m, W = self.m, self.W
+        step_ = max(1, min(count, (64 << 20) // (m * W * 4)))
+        packed = torch.empty(step_ * m * W, dtype=torch.int32, device=self.dev)
+        for a in range(first, first + count, step_):
+            c = min(step_, first + count - a)
+            # streams of slots [a, a + c), written from the start of `packed`
+            check(lib.hga_ref_init_packed(self.seed & MASK64, purpose, generation, a, c, m, packed.data_ptr(),
+                                          stream_ptr()),
+                  "hga_ref_init_packed")
+            check(lib.hga_unpack_i8(packed.data_ptr(), c, m, self.pop[buf][a].data_ptr(), stream_ptr()),
+                  "hga_unpack_i8")
+
+    def evaluate(self, buf: int, first: int, count: int) -> None:
+        fv = self.fit_var
+        out = self.fit[buf][first:first + count]
+        check(lib.hga_fitness_i8(self.pop[buf][first].data_ptr(), count, self.m, fv, ptr(out) if fv == 1 else None,
+                                 ptr(out) if fv == 2 else None, None, ptr(out) if fv == 8 else None, None,
+                                 self.fws.data_ptr(), self.fws.shape[0], stream_ptr()), "hga_fitness_i8")
+
+
+def _initial_state_i8(config: GAConfig, seed: int) -> SearchState:
+    res = _ResidentI8(config, seed)
+    total = config.total
+    res.init_slots(0, _P_INIT, 0, 0, total)
+    res.evaluate(0, 0, total)
+    best, idx = res.argmin(res.fit[0])
+    return SearchState(config, seed, res, 0, int(best), [int(best)], res.pop[0][idx].cpu().numpy())
+
+
+def _step_i8(state: SearchState) -> None:
+    """One reference generation on the int8 layout (engine.py:449-469)."""
+    res, cfg = state._res, state.config
+    gen = state.iteration + 1
+    N, m, half, total = res.N, res.m, 2 * res.N, 4 * res.N
+    cur, nxt = res.cur, res.cur ^ 1
+    sp = stream_ptr()
+    order = torch.empty(half, dtype=torch.int64, device=res.dev)
+    if _fitness_bound(m, res.fit_var) < int(lib.hga_select_max_range()):
+        flag = _dev.new_flag()
+        check(lib.hga_select_order(res.fit[cur].data_ptr(), total, order.data_ptr(), flag.data_ptr(),
+                                   res.sel_ws.data_ptr(), res.sel_ws.shape[0], sp), "hga_select_order")
+    else:
+        _select_radix(res.fit[cur], total, half, order)
+    perm = torch.empty(half, dtype=torch.int64, device=res.dev)
+    check(lib.hga_ref_permutation(state.seed, _sid(_P_SELECT, gen), 0, half, perm.data_ptr(), res.perm_ws.data_ptr(),
+                                  res.perm_ws.shape[0], sp), "hga_ref_permutation")
+    check(lib.hga_compose_gather(order.data_ptr(), perm.data_ptr(), half, res.pop[cur].data_ptr(),
+                                 res.pop[nxt].data_ptr(), m * m, res.fit[cur].data_ptr(), res.fit[nxt].data_ptr(),
+                                 None, sp), "hga_compose_gather")
+    from .rand import device_uniform
+
+    points = device_uniform(state.seed, _sid(_P_CROSSOVER, gen), 0, 1, m - 1, N)
+    flag = _dev.new_flag()
+    check(lib.hga_crossover_i8(res.pop[nxt].data_ptr(), total, m, points.data_ptr(), flag.data_ptr(), sp),
+          "hga_crossover_i8")
+    cols, ra, rb = _plan_device(cfg, state.seed, gen)
+    check(lib.hga_mutate_i8(res.pop[nxt].data_ptr(), total, m, cols.data_ptr(), ra.data_ptr(), rb.data_ptr(),
+                            cols.shape[1], ra.shape[1], flag.data_ptr(), sp), "hga_mutate_i8")
+    res.evaluate(nxt, half, half)
+    res.cur = nxt
+    fmin, idx = res.argmin(res.fit[nxt])
+    _check_flag(flag, "step")
+    state.iteration = gen
+    state.trace.append(fmin)
+    if fmin < state.best_fitness:
+        state.best_fitness = fmin
+        state.best_matrix = res.pop[nxt][idx].cpu().numpy()
+
+
+def _reinitialize_offspring_i8(state: SearchState) -> None:
+    res = state._res
+    half, total = 2 * res.N, 4 * res.N
+    res.init_slots(res.cur, _P_RESTART, state.iteration, half, half)
+    res.evaluate(res.cur, half, half)
+    fmin, idx = res.argmin(res.fit[res.cur][:total])
+    if fmin < state.best_fitness:
+        state.best_fitness = fmin
+        state.best_matrix = res.pop[res.cur][idx].cpu().numpy()
+
+
 def _step_reference(state: SearchState) -> None:
     res, cfg = state._res, state.config
     gen = state.iteration + 1
@@ -604,8 +731,11 @@ def _step_reference(state: SearchState) -> None:
         pwsb = int(lib.hga_ref_permutation_ws_bytes(half))
         res.perm_ws = torch.empty(max(pwsb, 1), dtype=torch.uint8, device=dev)
     flag = _dev.new_flag()
-    check(lib.hga_select_order(res.fit[cur].data_ptr(), total, order.data_ptr(), flag.data_ptr(),
-                               res.sel_ws.data_ptr(), res.sel_ws.shape[0], sp), "hga_select_order")
+    if _fitness_bound(m, res.fit_var) < int(lib.hga_select_max_range()):
+        check(lib.hga_select_order(res.fit[cur].data_ptr(), total, order.data_ptr(), flag.data_ptr(),
+                                   res.sel_ws.data_ptr(), res.sel_ws.shape[0], sp), "hga_select_order")
+    else:  # SQ at large orders: the value span may exceed the histogram
+        _select_radix(res.fit[cur], total, half, order)
     perm = torch.empty(half, dtype=torch.int64, device=dev)
     check(lib.hga_ref_permutation(state.seed, _sid(_P_SELECT, gen), 0, half, perm.data_ptr(), res.perm_ws.data_ptr(),
                                   res.perm_ws.shape[0], sp), "hga_ref_permutation")
@@ -678,7 +808,9 @@ def step(state, workers: int = 1):
     """
     if not isinstance(state, SearchState):
         return _step_host(state)
-    if state.config.rng == "reference":
+    if isinstance(state._res, _ResidentI8):
+        _step_i8(state)
+    elif state.config.rng == "reference":
         _step_reference(state)
     else:
         res = state._res
@@ -984,7 +1116,7 @@ def run_search(config: GAConfig, workers: int = 1, poll_interval: int = 256) -> 
     start = time.perf_counter()
     state = initial_state(config, workers=workers)
     complete = True
-    if config.rng == "reference":
+    if config.rng == "reference" or isinstance(state._res, _ResidentI8):
         last_restart = 0
         while state.iteration < config.max_iterations and state.best_fitness > 0:
             if config.time_budget_secs is not None and time.perf_counter() - start > config.time_budget_secs:
@@ -994,7 +1126,10 @@ def run_search(config: GAConfig, workers: int = 1, poll_interval: int = 256) -> 
             if (config.stall_window is not None and state.best_fitness > 0
                     and state.iteration - last_restart >= config.stall_window
                     and detect_stall(state, config.stall_window)):
-                _reinitialize_offspring(state)
+                if isinstance(state._res, _ResidentI8):
+                    _reinitialize_offspring_i8(state)
+                else:
+                    _reinitialize_offspring(state)
                 last_restart = state.iteration
     else:
         while state.iteration < config.max_iterations and state.best_fitness > 0:

@@ -58,7 +58,8 @@ def main():
             verified = bool((g == args.order * np.eye(args.order, dtype=np.int64)).all())
             verified &= int(oracle.penalties(q[None])[0, 1]) == 0 and bool(hga.is_balanced(q))
         line = {"order": args.order, "N": args.population, "matrices": 4 * args.population, "seed": seed,
-                "fitness": args.fitness, "nc": args.nc, "nr": args.nr, "stall_window": args.stall,
+                "fitness": args.fitness, "mutation": args.mutation, "nc": args.nc, "nr": args.nr,
+                "stall_window": args.stall,
                 "success": ok, "verified_HtH_eq_mI": verified, "generations": rec.iterations,
                 "best_fitness": rec.best_fitness, "wall_seconds": rec.wall_seconds,
                 "offspring_evals_per_s": 2 * args.population * rec.iterations / max(rec.wall_seconds, 1e-9),

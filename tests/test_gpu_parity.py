@@ -239,6 +239,25 @@ def test_select_device_ties_and_large(cuda_device):
         assert np.array_equal(tf.cpu().numpy(), want_f)
 
 
+def test_select_any_int64_range_matches_reference(cuda_device):
+    """The reference sorts any int64 fitness (stable argsort, engine.py:245);
+    spans beyond the histogram fall back to a stable radix sort."""
+    rng = np.random.default_rng(8)
+    for total, m, lo, hi in [(4000, 12, -(1 << 40), 1 << 40), (1000, 8, 0, 1 << 23), (6000, 16, -(1 << 62), 1 << 62)]:
+        pop = oracle.random_balanced(m, total, 5, 1, 0, 0)
+        fit = rng.integers(lo, hi, size=total, dtype=np.int64)
+        fit[::7] = fit[3]  # ties across the whole range
+        want_p, want_f = pop.copy(), fit.copy()
+        oracle.select(want_p, want_f, 9, engine._sid(2, 3))
+        assert sorted(want_f[: total // 2].tolist()) == np.sort(fit)[: total // 2].tolist()
+        for host in (True, False):
+            p, f = (pop.copy(), fit.copy()) if host else (torch.from_numpy(pop).cuda(), torch.from_numpy(fit).cuda())
+            hga.select(p, f, RngStream(9, engine._sid(2, 3)))
+            p = p if host else p.cpu().numpy()
+            f = f if host else f.cpu().numpy()
+            assert np.array_equal(p, want_p) and np.array_equal(f, want_f), (total, host)
+
+
 @pytest.mark.parametrize("m", [8, 12, 20, 36])
 def test_crossover_mutation_golden(golden, m, cuda_device):
     tag = f"xo_m{m}"

@@ -357,3 +357,73 @@ def test_device_invariant_check_counts_violations(cuda_device, monkeypatch):
     pop.copy_(saved)
     res.fit[res.cur].copy_(fsaved)
     assert engine.check_invariants(st) == (0, 0, 0)
+
+
+@pytest.mark.parametrize("m,N,fit,nc,nr", [(68, 300, "f2", 2, 3), (96, 200, "f1", 1, 4), (128, 150, "f2", 3, 2),
+                                           (36, 500, "sq", 2, 3), (48, 300, "sq", 1, 5), (64, 200, "sq", 2, 2)])
+def test_v1_loop_orders_and_sq(m, N, fit, nc, nr, cuda_device):
+    """Orders 68..128 and SQ above order 32 run the round-1 loop kernel (k_run,
+    generation.cu) instead of k_run_v3: invariants, fitness == oracle and the
+    exact survivor set after single steps, plus a multi-generation launch."""
+    cfg = engine.GAConfig(order=m, population=N, seed=19, fitness=fit, mutation_cols=nc, mutation_row_pairs=nr,
+                          max_iterations=10_000)
+    st = hga.initial_state(cfg)
+    rng = np.random.default_rng(m)
+    _device_invariants(st, None, rng)
+    for _ in range(3):
+        _check_selection_step(st)
+        _device_invariants(st, None, rng)
+    engine._run_device(st, 20, force=True)
+    _device_invariants(st, None, rng)
+    assert engine.check_invariants(st) == (0, 0, 0)
+    assert all(a >= b for a, b in zip(st.trace, st.trace[1:])) and st.iteration == 23
+
+
+def test_repeated_runs_are_bit_identical(cuda_device, monkeypatch):
+    """Race smoke test (compute-sanitizer is closed on this pool): the
+    hand-synchronised kernels -- the tcgen05 fitness pipeline (mbarrier rings,
+    TMEM slots, shared-memory finalisation ring) and the persistent loop
+    (one-atomic grid barrier, survivor lists) -- give bit-identical results
+    over repeated runs on the same inputs, at sizes with many units / tiles
+    per CTA."""
+    monkeypatch.setenv("HGA_FITNESS_TC", "2")
+    for m in (44, 48, 60, 64):
+        pop = engine.init_population_device(engine.GAConfig(order=m, population=60_000, seed=m))
+        ref = hga.penalties(pop)
+        for _ in range(4):
+            got = hga.penalties(pop)
+            for k in ("f1", "f2", "orth", "sq"):
+                assert torch.equal(got[k], ref[k]), (m, k)
+    monkeypatch.delenv("HGA_FITNESS_TC")
+    for m, N in ((20, 10_000), (36, 50_000)):
+        outs = []
+        for _ in range(3):
+            st = hga.initial_state(engine.GAConfig(order=m, population=N, seed=5, fitness="f2", mutation_cols=2,
+                                                   mutation_row_pairs=3, max_iterations=10_000))
+            engine._run_device(st, 30, force=True)
+            outs.append((list(st.trace), _hash_records(st._res.pop[st._res.cur].view(4 * N, -1)).sum().item(),
+                         st.fitness_device.sum().item()))
+        assert outs[0] == outs[1] == outs[2], m
+
+
+@pytest.mark.parametrize("m,N,fit,mut", [(132, 24, "f2", "multi"), (160, 12, "f1", "per-matrix"),
+                                         (256, 6, "f2", "shared")])
+def test_orders_above_128_run_the_reference_generation(m, N, fit, mut, cuda_device):
+    """Orders above the packed loops' 128 (the reference allows 4096,
+    engine.py:57): the int8-layout path reproduces the reference step for
+    step -- initial population, three generations and a stall restart."""
+    cfg = engine.GAConfig(order=m, population=N, seed=23, fitness=fit, mutation=mut, mutation_cols=2,
+                          mutation_row_pairs=3, max_iterations=6, stall_window=1)
+    st = hga.initial_state(cfg)
+    ref = oracle.initial_state(m, N, 23, fit, 2 if mut == "multi" else 1, 3 if mut == "multi" else 1, mut)
+    assert np.array_equal(st.population, ref.population) and np.array_equal(st.fitness, ref.fitness)
+    for _ in range(3):
+        hga.step(st)
+        oracle.step(ref)
+        assert np.array_equal(st.population, ref.population) and np.array_equal(st.fitness, ref.fitness)
+    assert st.trace == ref.trace and st.best_fitness == ref.best_fitness
+    rec = hga.run_search(cfg)
+    want = oracle.run_search(m, N, 23, fit, 2 if mut == "multi" else 1, 3 if mut == "multi" else 1, mut,
+                             max_iterations=6, stall_window=1)
+    assert rec.trace == want["trace"] and rec.iterations == want["iterations"]
+    assert np.array_equal(rec.best_matrix, want["best_matrix"])
