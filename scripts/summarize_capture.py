@@ -50,6 +50,7 @@ def raw(rep):
 
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__pipe_tensor_subpipe_imma_cycles_active.avg",
         "sm__cycles_elapsed.avg", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__registers_per_thread", "launch__grid_size",
@@ -72,7 +73,8 @@ for rep, m in (("fit_tc48.ncu-rep", 48), ("fit_tc64.ncu-rep", 64)):
     rd = to_bytes(*d["dram__bytes_read.sum"])
     wr = to_bytes(*d["dram__bytes_write.sum"])
     alg = n * (m * m + 8)
-    json.dump({"kernel": f"k_fit_i8_tc<{m},F2> (tcgen05.mma.kind::i8 column Gram, {n:,} int8 {m}x{m} matrices)",
+    json.dump({"kernel": f"{'k_fit_i8_tc2' if pre >= 'r02' else 'k_fit_i8_tc'}<{m},F2> (tcgen05.mma.kind::i8 column Gram, "
+                         f"{n:,} int8 {m}x{m} matrices)",
                "source": f"ncu --set full --clock-control none, `python scripts/prof_tc.py {m} {n}`; {src}/{rep}",
                "metrics": met, "algorithmic_bytes": alg, "dram_bytes": rd + wr, "traffic_over_algorithmic": (rd + wr) / alg,
                "evals_per_s_under_ncu": n / (t_us * 1e-6), "achieved_GBps": alg / (t_us * 1e-6) / 1e9,
