@@ -38,6 +38,10 @@ constexpr int kR2MaxGrid = 2048;
 constexpr int kR2MaxPlan = 128;  // nc + 2 nr <= (m - 1) + m
 constexpr int kRng = 64;          // items per key range (one-barrier select)
 constexpr int kMaxRng = 2048;     // one-barrier select up to 4N = 131,072 matrices
+// internal run flags (experiments): L2 bulk prefetch at launch of the population / of fitness + histogram
+constexpr uint32_t kRunPrefetchPop = 1u << 20;
+constexpr uint32_t kRunPrefetchFit = 1u << 21;
+constexpr uint32_t kRunPlainLaunch = 1u << 22;
 
 // Per-slot state: the two-barrier loop uses slots gen & 1, the one-barrier
 // loop gen % 3 (see k_run_v3).
@@ -966,12 +970,13 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
 
     int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
     int parity = (int)A.state[3];
-    {
+    if (A.flags & (kRunPrefetchPop | kRunPrefetchFit)) {
         // Cold launches (one generation per launch, L2 flushed by whatever ran before):
-        // bulk-prefetch the current population, its fitness and the select histogram
-        // into L2 at once, spread over all CTAs, so the dependent reads of the first
-        // generation hit L2 instead of paying an HBM round trip each.
-        const int64_t pieces[3] = {total * (int64_t)G::MW * 4, total * 8, (int64_t)kR2Bins * 4};
+        // bulk-prefetch the current population and / or its fitness + the select
+        // histogram into L2 at once, spread over all CTAs (experiment flags).
+        const int64_t pieces[3] = {(A.flags & kRunPrefetchPop) ? total * (int64_t)G::MW * 4 : 0,
+                                   (A.flags & kRunPrefetchFit) ? total * 8 : 0,
+                                   (A.flags & kRunPrefetchFit) ? (int64_t)kR2Bins * 4 : 0};
         const char* bases[3] = {reinterpret_cast<const char*>(A.pop[parity]),
                                 reinterpret_cast<const char*>(A.fit[parity]),
                                 reinterpret_cast<const char*>(&ws->hist[ONE ? (int)((iter + 1) % 3) : (int)((iter + 1) & 1)][0])};
@@ -1420,6 +1425,8 @@ int launch_run_v2_k(const hga_run_args* a, cudaStream_t st) {
     if (per_sm < 1) return HGA_E_UNSUPPORTED;
     const int grid = std::min(std::min(sm_count_cached() * std::min(per_sm, 2), kMaxNb), GROUPS * kR2Threads);
     void* params[] = {&P};
+    if (a->flags & kRunPlainLaunch)  // experiment: ordinary launch (co-residency by construction: grid <= resident CTAs)
+        return to_rc(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(kR2Threads * GROUPS), params, smem, st));
     return to_rc(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kR2Threads * GROUPS), params, smem, st));
 }
 
