@@ -74,9 +74,10 @@ def probe_fitness(quick):
                 o = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(4)]
             ptrs = [x.data_ptr() if x is not None else None for x in o]
             tc = m <= 64
-            for path in (("tcgen05", "popc") if tc else ("popc",)):
+            paths = (("tcgen05_r2", "tcgen05", "popc") if 36 <= m <= 64 else ("tcgen05", "popc")) if tc else ("popc",)
+            for path in paths:
                 if tc:
-                    os.environ["HGA_FITNESS_TC"] = "0" if path == "popc" else "all"
+                    os.environ["HGA_FITNESS_TC"] = {"popc": "0", "tcgen05": "all", "tcgen05_r2": "2"}[path]
                 t = timed(lambda: lib.hga_fitness_i8(pop.data_ptr(), n, m, var, *ptrs, None, None, 0, st))
                 os.environ.pop("HGA_FITNESS_TC", None)
                 bytes_ = n * (m * m + 8 * bin(var).count("1"))
