@@ -266,11 +266,12 @@ int hga_run(const hga_run_args *args, void *stream);
  * dev_i8 is a device int8 staging buffer of 4N*m*m
  * bytes.  On return (copy_stream synchronised) host_pop/host_fit hold the new
  * population, state_out[0..7] the device state after the generation and
- * *flag_out the HGA_FLAG_* bits.  The population is validated after the
- * upload (one host synchronisation): when HGA_FLAG_NOT_SIGN (an entry is not
- * +-1) or HGA_FLAG_NOT_GA (column 0 not all +1, or an unbalanced column) is
- * set, nothing runs, host_pop/host_fit are left untouched and the caller
- * takes the exact explicit-plan path instead. */
+ * *flag_out the HGA_FLAG_* bits.  The pack validates the upload on the
+ * device: when HGA_FLAG_NOT_SIGN (an entry is not +-1) or HGA_FLAG_NOT_GA
+ * (column 0 not all +1, or an unbalanced column) is set, the generation and
+ * the unpack do nothing and host_pop/host_fit get their own values back
+ * (no host round trip mid-step); the caller then raises or takes the exact
+ * explicit-plan path. */
 int hga_step_host(const hga_run_args *args, int8_t *host_pop, int64_t *host_fit, int8_t *dev_i8,
                   const int64_t *state_in, int64_t *state_out, int32_t *flag_out, int32_t chunks,
                   void *stream, void *copy_stream);

@@ -313,7 +313,10 @@ __global__ void k_pack_quads(const int8_t* __restrict__ pop, int64_t n, int m, u
 // r's bit from each column word (neighbouring rows share the words through
 // L1) and writes the row as m / 4 four-byte stores.
 __global__ void k_unpack_rows(const uint32_t* __restrict__ cols, int64_t n, int m, int W,
-                              int8_t* __restrict__ pop) {
+                              int8_t* __restrict__ pop, const int32_t* __restrict__ skip_if = nullptr) {
+    // skip_if (hga_step_host): a rejected upload leaves the staging bytes (the
+    // caller's own population) in place
+    if (skip_if && (*skip_if & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA))) return;
     const int64_t rows = n * m;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = t / m;
@@ -406,6 +409,14 @@ static int grid_for(int64_t work, int threads) {
     int64_t g = (work + threads - 1) / threads;
     int64_t cap = (int64_t)sm_count_cached() * 16;
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, cap));
+}
+
+// hga_step_host's guarded unpack (m % 4 == 0, 4-byte aligned staging): no-op when the
+// uploaded population was rejected
+int unpack_i8_guarded(const uint32_t* cols, int64_t n, int32_t m, int8_t* pop, const int32_t* flag, cudaStream_t st) {
+    if (n <= 0) return HGA_OK;
+    k_unpack_rows<<<grid_for(n * (int64_t)m, 256), 256, 0, st>>>(cols, n, m, words_for(m), pop, flag);
+    return to_rc(cudaGetLastError());
 }
 
 }  // namespace hga

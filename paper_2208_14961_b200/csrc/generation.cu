@@ -673,6 +673,16 @@ static int run2_prepare(const hga_run_args* a, cudaStream_t st) {
 }  // namespace hga
 
 namespace hga {
+int unpack_i8_guarded(const uint32_t* cols, int64_t n, int32_t m, int8_t* pop, const int32_t* flag, cudaStream_t st);
+
+// hga_step_host on a rejected upload: the fitness copy-back returns the uploaded values
+__global__ void k_fit_restore_if(const int64_t* __restrict__ src, int64_t* __restrict__ dst, int64_t n,
+                                 const int32_t* __restrict__ flag) {
+    if (!(*flag & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA))) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 // state block of a host-driven step: iteration, best, last restart, parity 0,
 // best index 0, stop 0, run length, last trace value
 __global__ void k_set_state(int64_t* s, int64_t it, int64_t best, int64_t last_restart, int64_t run, int64_t last) {
@@ -811,32 +821,35 @@ int hga_step_host(const hga_run_args* a, int8_t* host_pop, int64_t* host_fit, in
         if (rc) return done(rc);
     }
     if (e != cudaSuccess) return done(to_rc(e));
-    // validate before anything is computed: the loop's fast paths need the GA
-    // invariants (column 0 skipped in the pair chain, fitness >> granule keys);
-    // on a violation the host arrays stay untouched and the caller runs the
-    // exact explicit-plan generation instead
-    e = cudaMemcpyAsync(flag_out, dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return done(to_rc(e));
-    if (*flag_out & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA)) return HGA_OK;
+    // The pack validated the upload (dflag): the loop's fast paths need the GA
+    // invariants (column 0 skipped in the pair chain, fitness >> granule keys).
+    // On a violation the generation and the unpack do nothing and the fitness
+    // copy-back returns the uploaded values, so the host arrays get their own
+    // bytes back; the caller then runs the exact explicit-plan generation.
+    // Decided on the device: no host round trip in the middle of the step.
     if (tm) cudaEventRecord(te[1], cs);
     if (tm) cudaEventRecord(te[2], st);
     k_set_state<<<1, 8, 0, st>>>(a->state, state_in[0], state_in[1], state_in[2], state_in[6], state_in[7]);
     hga_run_args r = *a;
     r.gens_this_call = 1;
-    r.flags |= HGA_RUN_FORCE;  // exactly one generation: the new population is in buffer 1
+    r.flags |= HGA_RUN_FORCE | kRunHostCheck;  // exactly one generation: the new population is in buffer 1
     int rc = hga_run_prepare(&r, st);
     if (!rc) rc = hga_run(&r, st);
     if (rc) return done(rc);
     if (tm) cudaEventRecord(te[3], st);
     for (int i = 0; i < k && e == cudaSuccess; ++i) {
         const int64_t lo = total * i / k, hi = total * (i + 1) / k;
-        rc = hga_unpack_i8(a->pop[1] + lo * mw, hi - lo, m, dev_i8 + lo * mm, st);
+        rc = unpack_i8_guarded(a->pop[1] + lo * mw, hi - lo, m, dev_i8 + lo * mm, dflag, st);
         if (rc) return done(rc);
         e = cudaEventRecord(ev[k + i], st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[k + i], 0);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(host_pop + lo * mm, dev_i8 + lo * mm, (hi - lo) * mm, cudaMemcpyDeviceToHost, cs);
+    }
+    if (e == cudaSuccess) {
+        k_fit_restore_if<<<(unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count_cached() * 4), 256, 0,
+                           st>>>(a->fit[0], a->fit[1], total, dflag);
+        e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaEventRecord(ev[2 * k + 1], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[2 * k + 1], 0);

@@ -42,6 +42,9 @@ constexpr int kMaxRng = 2048;     // one-barrier select up to 4N = 131,072 matri
 constexpr uint32_t kRunPrefetchPop = 1u << 20;
 constexpr uint32_t kRunPrefetchFit = 1u << 21;
 constexpr uint32_t kRunPlainLaunch = 1u << 22;
+// internal (hga_step_host): do nothing when the uploaded population was rejected
+// (RunWs2::host_flag has HGA_FLAG_NOT_SIGN / HGA_FLAG_NOT_GA) -- no host round trip
+constexpr uint32_t kRunHostCheck = 1u << 23;
 
 // Per-slot state: the two-barrier loop uses slots gen & 1, the one-barrier
 // loop gen % 3 (see k_run_v3).
@@ -968,6 +971,8 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     TileSharedTP* T1 = reinterpret_cast<TileSharedTP*>(gbase + 2 * kRowsBytes + kTPS);
     int8_t* tplan = reinterpret_cast<int8_t*>(gbase + 2 * kRowsBytes + 2 * kTPS);
 
+    if ((A.flags & kRunHostCheck) && (__ldcg(&ws->host_flag) & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA)))
+        return;  // uniform over the grid: no barrier has been entered
     int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
     int parity = (int)A.state[3];
     if (A.flags & (kRunPrefetchPop | kRunPrefetchFit)) {
