@@ -281,6 +281,9 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e through the public API with host (numpy) buffers
     e2e = run_e2e(args, cfg, hga, engine, torch)
+    # the same public call computing exactly what the reference arm computes:
+    # reference streams, the reference arm's seed and initial population
+    e2e_same = run_e2e_same_config(args, engine, torch) if not args.no_cpu else None
     # the same public call on the device-resident SearchState (each step reads
     # back its trace entry / best fitness): what run_search-style users get
     st2 = hga.initial_state(cfg)
@@ -326,6 +329,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roofline,
         "e2e": e2e,
         "e2e_resident": e2e_resident,
+        "e2e_same_config": e2e_same,
         "persistent_run": {"value": persistent * world, "unit": UNIT, "generations_per_launch": args.steps,
                            "note": "production run_search mode: K generations in one launch, L2 warm"},
         "wall_seconds_timed_region": wall,
@@ -377,6 +381,46 @@ def run_e2e(args, cfg, hga, engine, torch):
             "d2h_bytes_per_step": int(pop.nbytes + fit.nbytes + 8), "steps": steps, "ms_per_step": t * 1e3,
             "api": "paper_2208_14961_b200.engine.step(state) with numpy population/fitness (drop-in for "
                    "hadamard_ga.step; one hga_step_host call: H2D, pack, generation, chunked unpack + D2H)"}
+
+
+def run_e2e_same_config(args, engine, torch):
+    """engine.step() on a host state with rng="reference": the reference's
+    splitmix64 streams, seed 2024 and the oracle's initial population, i.e.
+    step for step the computation the reference arm (`--impl reference`)
+    times; the first step is checked bit for bit against the oracle."""
+    import oracle
+
+    @dataclass
+    class HostState:
+        config: object
+        seed: int
+        population: np.ndarray
+        fitness: np.ndarray
+        iteration: int
+        best_matrix: np.ndarray
+        best_fitness: int
+        trace: list = field(default_factory=list)
+
+    cfg = engine.GAConfig(order=ORDER, population=N_PAIRS, seed=2024, fitness=FITNESS, mutation_cols=NC,
+                          mutation_row_pairs=NR, max_iterations=engine.MAX_ITERATIONS, rng="reference")
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    ref = oracle.initial_state(ORDER, N_PAIRS, 2024, FITNESS, NC, NR, "multi", threads=threads)
+    hs = HostState(cfg, 2024, ref.population.copy(), ref.fitness.copy(), 0, ref.best_matrix.copy(),
+                   ref.best_fitness, [ref.best_fitness])
+    engine.step(hs)
+    oracle.step(ref, threads)
+    identical = bool(np.array_equal(hs.population, ref.population) and np.array_equal(hs.fitness, ref.fitness))
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 20))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        engine.step(hs)
+    t = (time.perf_counter() - t0) / steps
+    return {"value": 2 * N_PAIRS / t, "unit": UNIT, "h2d_bytes_per_step": int(hs.population.nbytes + hs.fitness.nbytes),
+            "d2h_bytes_per_step": int(hs.population.nbytes + hs.fitness.nbytes), "steps": steps, "ms_per_step": t * 1e3,
+            "rng": "reference", "seed": 2024, "identical_to_reference_arm_step1": identical,
+            "api": "engine.step(state) on numpy arrays with GAConfig(rng='reference'): the reference arm's streams, "
+                   "seed and initial population (explicit-plan kernels)"}
 
 
 def run_fitness_sweep(args, engine, torch, lib, peaks):

@@ -58,6 +58,9 @@ namespace tc2 {
 
 using namespace tcx;
 
+#ifndef HGA_TC2_SPIN
+#define HGA_TC2_SPIN 0  // 1: epilogue / MMA waits busy-poll (test_wait); 2: + check warps
+#endif
 #ifndef HGA_TC2_M128
 #define HGA_TC2_M128 0
 #endif
@@ -271,8 +274,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         int it = 0;
         for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
             const int ts = it % G::TSTAGES, a = it % kSlots;
-            mbar_wait(&tready[ts], (it / G::TSTAGES) & 1);
-            mbar_wait(&tempty[a], ((it / kSlots) & 1) ^ 1);
+            if constexpr (HGA_TC2_SPIN >= 1) {
+                mbar_wait_spin(&tready[ts], (it / G::TSTAGES) & 1);
+                mbar_wait_spin(&tempty[a], ((it / kSlots) & 1) ^ 1);
+            } else {
+                mbar_wait(&tready[ts], (it / G::TSTAGES) & 1);
+                mbar_wait(&tempty[a], ((it / kSlots) & 1) ^ 1);
+            }
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             if (lane == 0) {
                 const uint32_t st = sbase + (uint32_t)(ts * G::TSTAGE);
@@ -318,8 +326,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         int it = 0;
         for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
             const int rs = it % G::RSTAGES, ts = it % G::TSTAGES;
-            mbar_wait(&rfull[rs], (it / G::RSTAGES) & 1);
-            mbar_wait(&tfree[ts], ((it / G::TSTAGES) & 1) ^ 1);
+            if constexpr (HGA_TC2_SPIN >= 2) {
+                mbar_wait_spin(&rfull[rs], (it / G::RSTAGES) & 1);
+                mbar_wait_spin(&tfree[ts], ((it / G::TSTAGES) & 1) ^ 1);
+            } else {
+                mbar_wait(&rfull[rs], (it / G::RSTAGES) & 1);
+                mbar_wait(&tfree[ts], ((it / G::TSTAGES) & 1) ^ 1);
+            }
             const uint8_t* rawu = raw0 + rs * G::RSTAGE;
             uint8_t* tileu = smem + ts * G::TSTAGE;
             int sqa[kMpw][4], lna[kMpw][4];
@@ -396,7 +409,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             int it = 0;
             for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++it) {
                 const int a = it % kSlots, buf = it % kBufs;
-                mbar_wait(&tfull[a], (it / kSlots) & 1);
+                if constexpr (HGA_TC2_SPIN >= 1) mbar_wait_spin(&tfull[a], (it / kSlots) & 1);
+                else mbar_wait(&tfull[a], (it / kSlots) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t taddr = G::M128
                                            ? tbase + (uint32_t)(a * G::SLOT + g * 128 + 64 * (q >> 1)) + ((uint32_t)(32 * q) << 16)

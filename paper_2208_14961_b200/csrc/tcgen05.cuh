@@ -31,6 +31,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
 }
 
+// Busy-poll variant (mbarrier.test_wait never suspends the warp): for waits
+// on a short, latency-critical handshake where the suspend/wake-up of
+// try_wait would add to the chain.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SPIN_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SPIN_%=;\n}\n" ::"r"(saddr(b)),
+        "r"(parity)
+        : "memory");
+}
+
 __device__ __forceinline__ void cp_async_piece4(uint32_t dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
