@@ -276,6 +276,26 @@ int hga_step_host(const hga_run_args *args, int8_t *host_pop, int64_t *host_fit,
                   const int64_t *state_in, int64_t *state_out, int32_t *flag_out, int32_t chunks,
                   void *stream, void *copy_stream);
 
+/* hga_step_host with the population moved as a BIT STREAM (8x fewer PCIe
+ * bytes): the same step (engine.py:449-469) and the same contract as
+ * hga_step_host, for orders 4..64 with m % 4 == 0.  The host packs the
+ * caller's int8 bytes (validating every byte is +-1; AVX2 on a small host
+ * thread pool, HGA_HOST_THREADS) into host_bits -- bit e of the stream set
+ * iff byte e of host_pop is -1 -- piece by piece (`chunks` pieces), each
+ * piece uploaded as soon as it is packed; the device turns the stream into
+ * column records (and checks the GA invariants), runs the generation and
+ * turns the new population back into a stream, which is copied down piece
+ * by piece and unpacked into host_pop on the host as each piece lands.
+ * host_bits: PAGE-LOCKED host buffer, dev_bits: device buffer, each of
+ * hga_step_host_bits_bytes(n_pairs, m) bytes (0 = order not supported).
+ * A byte that is not +-1 returns with *flag_out = HGA_FLAG_NOT_SIGN before
+ * any device work that could touch the caller's arrays; HGA_FLAG_NOT_GA
+ * leaves host_pop as it was and host_fit holding its own values. */
+size_t hga_step_host_bits_bytes(int64_t n_pairs, int32_t m);
+int hga_step_host_bits(const hga_run_args *args, int8_t *host_pop, int64_t *host_fit, uint32_t *host_bits,
+                       uint32_t *dev_bits, const int64_t *state_in, int64_t *state_out, int32_t *flag_out,
+                       int32_t chunks, void *stream, void *copy_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,6 +18,7 @@
 //         parents copied to the new buffer (out-of-place gather, engine.py:247)
 //      F  trace / best / stop / stall-restart bookkeeping, replicated in every
 //         CTA from the same global values so all CTAs agree without a barrier
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -674,6 +675,13 @@ static int run2_prepare(const hga_run_args* a, cudaStream_t st) {
 
 namespace hga {
 int unpack_i8_guarded(const uint32_t* cols, int64_t n, int32_t m, int8_t* pop, const int32_t* flag, cudaStream_t st);
+// step_bits.cu / host_bits.cpp: the bit-stream transfer of hga_step_host_bits
+int bits_to_cols(const uint32_t* bits, int64_t n, int32_t m, uint32_t* cols, int32_t* flag, cudaStream_t st);
+int cols_to_bits(const uint32_t* cols, int64_t n, int32_t m, int64_t w0, int64_t w1, uint32_t* bits,
+                 const int32_t* skip, cudaStream_t st);
+int host_pack_bits(const int8_t* src, int64_t nbytes, uint32_t* dst, int64_t w0, int64_t w1);
+void host_unpack_bits(const uint32_t* src, int8_t* dst, int64_t nbytes, int64_t w0, int64_t w1);
+int host_pool_threads();
 
 // hga_step_host on a rejected upload: the fitness copy-back returns the uploaded values
 __global__ void k_fit_restore_if(const int64_t* __restrict__ src, int64_t* __restrict__ dst, int64_t n,
@@ -867,6 +875,119 @@ int hga_step_host(const hga_run_args* a, int8_t* host_pop, int64_t* host_fit, in
         for (auto& t : te) cudaEventDestroy(t);
     }
     return done(to_rc(e));
+}
+
+size_t hga_step_host_bits_bytes(int64_t n_pairs, int32_t m) {
+    if (n_pairs < 1 || m < 4 || m > 64 || (m & 3)) return 0;
+    const int64_t nbytes = 4 * n_pairs * (int64_t)m * m;
+    return (size_t)((nbytes + 31) / 32) * 4;
+}
+
+int hga_step_host_bits(const hga_run_args* a, int8_t* host_pop, int64_t* host_fit, uint32_t* host_bits,
+                       uint32_t* dev_bits, const int64_t* state_in, int64_t* state_out, int32_t* flag_out,
+                       int32_t chunks, void* stream, void* copy_stream) {
+    if (!run_args_ok(a) || !host_pop || !host_fit || !host_bits || !dev_bits || !state_in || !state_out || !flag_out ||
+        chunks < 1)
+        return HGA_E_INVALID;
+    if (!run2_supported(a) || (a->m & 3)) return HGA_E_UNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
+    const int m = a->m;
+    const int64_t total = 4 * a->n_pairs, nbytes = total * (int64_t)m * m, nwords = (nbytes + 31) / 32;
+    const int k = (int)std::min<int64_t>(std::min<int32_t>(chunks, 64), nwords);
+    int32_t* dflag = &reinterpret_cast<RunWs2*>(a->ws)->host_flag;
+    auto wlo = [&](int i) { return nwords * i / k; };
+    thread_local std::vector<cudaEvent_t> pool;  // see hga_step_host
+    while ((int)pool.size() < 2 * k + 4) {
+        cudaEvent_t ne;
+        const cudaError_t ce = cudaEventCreateWithFlags(&ne, cudaEventDisableTiming);
+        if (ce != cudaSuccess) return to_rc(ce);
+        pool.push_back(ne);
+    }
+    cudaEvent_t* ev = pool.data();  // [0..k) pieces copied down, k: buffers free, k+1: upload done, k+2: flag, k+3: end
+    const bool tm = std::getenv("HGA_STEP_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t0 = now();
+    *flag_out = 0;
+    // the device staging and the packed buffers are free once prior work on `stream` is done
+    cudaError_t e = cudaEventRecord(ev[k], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[k], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(a->fit[0], host_fit, total * sizeof(int64_t), cudaMemcpyHostToDevice, cs);
+    if (e != cudaSuccess) return to_rc(e);
+    // host: validate + pack piece i, then its upload goes out while piece i + 1 is packed
+    int bad = 0;
+    for (int i = 0; i < k && !bad; ++i) {
+        bad = host_pack_bits(host_pop, nbytes, host_bits, wlo(i), wlo(i + 1));
+        if (!bad)
+            e = cudaMemcpyAsync(dev_bits + wlo(i), host_bits + wlo(i), (wlo(i + 1) - wlo(i)) * 4, cudaMemcpyHostToDevice, cs);
+        if (e != cudaSuccess) return to_rc(e);
+    }
+    const auto t1 = now();
+    if (bad) {  // an entry is not +-1: nothing was written to the caller's arrays
+        e = cudaStreamSynchronize(cs);
+        *flag_out = HGA_FLAG_NOT_SIGN;
+        return to_rc(e);
+    }
+    e = cudaEventRecord(ev[k + 1], cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int32_t), st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[k + 1], 0);
+    if (e != cudaSuccess) return to_rc(e);
+    int rc = bits_to_cols(dev_bits, total, m, a->pop[0], dflag, st);
+    if (rc) return rc;
+    e = cudaEventRecord(ev[k + 2], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[k + 2], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(flag_out, dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[k + 2], cs);
+    if (e != cudaSuccess) return to_rc(e);
+    k_set_state<<<1, 8, 0, st>>>(a->state, state_in[0], state_in[1], state_in[2], state_in[6], state_in[7]);
+    hga_run_args r = *a;
+    r.gens_this_call = 1;
+    r.flags |= HGA_RUN_FORCE | kRunHostCheck;  // exactly one generation: the new population is in buffer 1
+    rc = hga_run_prepare(&r, st);
+    if (!rc) rc = hga_run(&r, st);
+    if (rc) return rc;
+    for (int i = 0; i < k && e == cudaSuccess; ++i) {
+        rc = cols_to_bits(a->pop[1], total, m, wlo(i), wlo(i + 1), dev_bits, dflag, st);
+        if (rc) return rc;
+        e = cudaEventRecord(ev[i], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[i], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(host_bits + wlo(i), dev_bits + wlo(i), (wlo(i + 1) - wlo(i)) * 4, cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[i], cs);
+    }
+    if (e == cudaSuccess) {
+        // a rejected population (NOT_GA): the fitness copy-back returns the uploaded values
+        k_fit_restore_if<<<(unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count_cached() * 4), 256, 0,
+                           st>>>(a->fit[0], a->fit[1], total, dflag);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(ev[k + 3], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[k + 3], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host_fit, a->fit[1], total * sizeof(int64_t), cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(state_out, a->state, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, cs);
+    if (e != cudaSuccess) return to_rc(e);
+    const auto t2 = now();
+    // host: the validation flag first (on NOT_GA the caller's population stays as it is), then
+    // unpack each piece as soon as it has landed while the later pieces are still in flight
+    e = cudaEventSynchronize(ev[k + 2]);
+    if (e != cudaSuccess) return to_rc(e);
+    const auto t3 = now();
+    if (!(*flag_out & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA))) {
+        for (int i = 0; i < k; ++i) {
+            e = cudaEventSynchronize(ev[i]);
+            if (e != cudaSuccess) return to_rc(e);
+            host_unpack_bits(host_bits, host_pop, nbytes, wlo(i), wlo(i + 1));
+        }
+    }
+    const auto t4 = now();
+    e = cudaStreamSynchronize(cs);
+    if (tm) {
+        auto us = [&](std::chrono::steady_clock::time_point x) {
+            return std::chrono::duration<double, std::micro>(x - t0).count();
+        };
+        std::fprintf(stderr, "hga_step_host_bits us: packed+uploads_enqueued %.1f enqueued %.1f flag %.1f unpacked %.1f done %.1f (%d host threads)\n",
+                     us(t1), us(t2), us(t3), us(t4), us(now()), host_pool_threads());
+    }
+    return to_rc(e);
 }
 
 int hga_philox_init_packed(uint64_t seed, uint64_t purpose, uint64_t generation, int64_t first_slot,

@@ -28,6 +28,7 @@ orthogonal column pairs), and `penalties` returns all four from one pass.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 import weakref
 from dataclasses import dataclass, field
@@ -37,8 +38,8 @@ import torch
 
 from . import _dev
 from ._dev import HgaError, check, lib, ptr, stream_ptr, words_for
-from ._lib import (FLAG_FIT_RANGE, FLAG_NOT_GA, FLAG_NOT_SIGN, FLAG_PLAN_RANGE, FLAG_POINT_RANGE, MUT_CODES, RUN_FORCE,
-                   RunArgs, VARIANT_BITS)
+from ._lib import (FLAG_FIT_RANGE, FLAG_NOT_GA, FLAG_NOT_SIGN, FLAG_PLAN_RANGE, FLAG_POINT_RANGE, HGA_E_UNSUPPORTED,
+                   MUT_CODES, RUN_FORCE, RunArgs, VARIANT_BITS)
 from .rand import MASK64, RngStream, random_seed
 
 __all__ = [
@@ -856,6 +857,19 @@ class _HostBridge:
         self.host_state_in = torch.empty(8, dtype=torch.int64, pin_memory=True)  # pinned: no hidden stream sync
         self.host_flag = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.args = None
+        self._bits = None
+
+    def bit_buffers(self):
+        """(page-locked host, device) staging of hga_step_host_bits, or None
+        when the order has no bit-stream path (or HGA_STEP_HOST=bytes)."""
+        if self._bits is None:
+            nb = int(lib.hga_step_host_bits_bytes(self.cfg.population, self.cfg.order))
+            if nb == 0 or os.environ.get("HGA_STEP_HOST", "") == "bytes":
+                self._bits = False
+            else:
+                self._bits = (torch.empty(nb, dtype=torch.uint8, pin_memory=True),
+                              torch.empty(nb, dtype=torch.uint8, device=self.res.dev))
+        return self._bits or None
 
     def pin(self, arr: np.ndarray) -> None:
         """Page-lock `arr` in place; not fatal when the runtime refuses (already
@@ -890,6 +904,7 @@ def _unregister_all(registered: dict) -> None:
     registered.clear()
 
 
+_BIT_CHUNKS = 4  # pieces of the bit-stream upload / download (hga_step_host_bits)
 _HOST_CHUNKS = 8  # host <-> device population copies are pipelined against pack / unpack in this many pieces
 
 
@@ -959,9 +974,22 @@ def _step_host(state):
             bridge.hs_np, bridge.hf_np = bridge.host_state.numpy(), bridge.host_flag.numpy()
         st_in = bridge.st_in
         st_in[0], st_in[1], st_in[2], st_in[6], st_in[7] = it0, best0, 0, 1, last0
-        check(lib.hga_step_host(bridge.args, pop_np.ctypes.data, fit_np.ctypes.data, bridge.pop_i8.data_ptr(), st_in,
-                                bridge.host_state.data_ptr(), bridge.host_flag.data_ptr(), _HOST_CHUNKS,
-                                stream_ptr(), bridge.copy_stream.cuda_stream), "hga_step_host")
+        bits = bridge.bit_buffers()
+        if bits is not None:
+            # the population crosses PCIe as a bit stream (hga_step_host_bits: 8x fewer bytes)
+            rc = lib.hga_step_host_bits(bridge.args, pop_np.ctypes.data, fit_np.ctypes.data, bits[0].data_ptr(),
+                                        bits[1].data_ptr(), st_in, bridge.host_state.data_ptr(),
+                                        bridge.host_flag.data_ptr(), _BIT_CHUNKS, stream_ptr(),
+                                        bridge.copy_stream.cuda_stream)
+        else:
+            rc = lib.hga_step_host(bridge.args, pop_np.ctypes.data, fit_np.ctypes.data, bridge.pop_i8.data_ptr(),
+                                   st_in, bridge.host_state.data_ptr(), bridge.host_flag.data_ptr(), _HOST_CHUNKS,
+                                   stream_ptr(), bridge.copy_stream.cuda_stream)
+        if rc == HGA_E_UNSUPPORTED:  # the v1 loop's configs (SQ above 32, m % 4 != 0, long plans): generic path
+            _step_host_generic(state, bridge, pop_np, fit_np, it0, best0, last0, explicit)
+            _write_back(state, pop_np, fit_np)
+            return state
+        check(rc, "hga_step_host")
         hf = int(bridge.hf_np[0])
         if hf & FLAG_NOT_SIGN:
             raise ValueError("step: matrix entries must be +1 or -1")

@@ -427,3 +427,39 @@ def test_orders_above_128_run_the_reference_generation(m, N, fit, mut, cuda_devi
                              max_iterations=6, stall_window=1)
     assert rec.trace == want["trace"] and rec.iterations == want["iterations"]
     assert np.array_equal(rec.best_matrix, want["best_matrix"])
+
+
+# ------------------------------------------------------------ bit-stream host step
+
+
+@pytest.mark.parametrize("m,N,fit,nc,nr", [(4, 3, "f1", 1, 1), (20, 10_000, "f2", 4, 2), (36, 500, "f2", 1, 12),
+                                           (48, 257, "f1", 2, 3), (64, 300, "f2", 3, 5), (12, 40, "sq", 2, 2),
+                                           (36, 64, "sq", 2, 2)])
+def test_host_step_bit_stream_matches_byte_path(m, N, fit, nc, nr, cuda_device, monkeypatch):
+    """hga_step_host_bits (population moved as a bit stream, packed and
+    unpacked on the host) gives exactly the populations, fitness and traces
+    of the int8 path (hga_step_host) step after step; configs outside the
+    loop's fast path (SQ above 32) take the generic path on both."""
+    cfg = engine.GAConfig(order=m, population=N, seed=17, fitness=fit, mutation_cols=nc, mutation_row_pairs=nr)
+    pop = oracle.init_population(m, N, 17)
+    f = oracle.evaluate(pop, fit)
+    a = _host_state(cfg, 17, pop.copy(), f.copy())
+    b = _host_state(cfg, 17, pop.copy(), f.copy())
+    monkeypatch.delenv("HGA_STEP_HOST", raising=False)
+    hga.step(a)
+    monkeypatch.setenv("HGA_STEP_HOST", "bytes")
+    hga.step(b)
+    monkeypatch.delenv("HGA_STEP_HOST")
+    has_bits = int(engine.lib.hga_step_host_bits_bytes(N, m)) > 0
+    assert bool(a._hga_bridge._bits) == has_bits and b._hga_bridge._bits is False
+    for i in range(4):
+        assert np.array_equal(a.population, b.population), i
+        assert np.array_equal(a.fitness, b.fitness), i
+        assert a.trace == b.trace and a.iteration == b.iteration == i + 1
+        hga.step(a)
+        hga.step(b)
+    assert np.array_equal(a.population, b.population) and np.array_equal(a.fitness, b.fitness)
+    p = a.population
+    assert (p[:, :, 0] == 1).all() and (p[:, :, 1:].sum(axis=1) == 0).all()
+    sample = np.arange(0, 4 * N, max(1, 4 * N // 4000))
+    assert np.array_equal(a.fitness[sample], oracle.evaluate(p[sample], fit))
