@@ -377,10 +377,20 @@ def run_e2e(args, cfg, hga, engine, torch):
         engine.step(hs)
     t = (time.perf_counter() - t0) / steps
     assert hs.population[:, :, 0].min() == 1
-    return {"value": 2 * N_PAIRS / t, "unit": UNIT, "h2d_bytes_per_step": int(pop.nbytes + fit.nbytes + 64),
-            "d2h_bytes_per_step": int(pop.nbytes + fit.nbytes + 8), "steps": steps, "ms_per_step": t * 1e3,
-            "api": "paper_2208_14961_b200.engine.step(state) with numpy population/fitness (drop-in for "
-                   "hadamard_ga.step; one hga_step_host call: H2D, pack, generation, chunked unpack + D2H)"}
+    bridge = hs._hga_bridge
+    if bridge.bit_buffers() is not None:  # the population crosses PCIe as a bit stream
+        stream_bytes = (pop.nbytes + 31) // 32 * 4
+        api = ("paper_2208_14961_b200.engine.step(state) with numpy population/fitness (drop-in for hadamard_ga.step; "
+               "one hga_step_host_bits call: host AVX2 pack + validation of the int8 population into a bit stream "
+               "(8x fewer PCIe bytes) pipelined with its upload and the device stream->column kernels, one CUDA "
+               "graph for the generation and the piecewise download, host unpack as the pieces land)")
+    else:
+        stream_bytes = pop.nbytes
+        api = ("paper_2208_14961_b200.engine.step(state) with numpy population/fitness (drop-in for "
+               "hadamard_ga.step; one hga_step_host call: H2D, pack, generation, chunked unpack + D2H)")
+    return {"value": 2 * N_PAIRS / t, "unit": UNIT, "h2d_bytes_per_step": int(stream_bytes + fit.nbytes + 64),
+            "d2h_bytes_per_step": int(stream_bytes + fit.nbytes + 68), "steps": steps, "ms_per_step": t * 1e3,
+            "host_population_bytes": int(pop.nbytes), "api": api}
 
 
 def run_e2e_same_config(args, engine, torch):

@@ -28,6 +28,7 @@
 #include "run_v2.cuh"
 
 #include <cstddef>
+#include <cstring>
 
 namespace hga {
 
@@ -677,10 +678,11 @@ namespace hga {
 int unpack_i8_guarded(const uint32_t* cols, int64_t n, int32_t m, int8_t* pop, const int32_t* flag, cudaStream_t st);
 // step_bits.cu / host_bits.cpp: the bit-stream transfer of hga_step_host_bits
 int bits_to_cols(const uint32_t* bits, int64_t n, int32_t m, uint32_t* cols, int32_t* flag, cudaStream_t st);
-int cols_to_bits(const uint32_t* cols, int64_t n, int32_t m, int64_t w0, int64_t w1, uint32_t* bits,
-                 const int32_t* skip, cudaStream_t st);
-int host_pack_bits(const int8_t* src, int64_t nbytes, uint32_t* dst, int64_t w0, int64_t w1);
-void host_unpack_bits(const uint32_t* src, int8_t* dst, int64_t nbytes, int64_t w0, int64_t w1);
+int cols_to_bits(const uint32_t* cols, int64_t n, int32_t m, uint32_t* bits, const int32_t* skip, cudaStream_t st);
+int host_pack_pieces(const int8_t* src, int64_t nbytes, uint32_t* dst, const int64_t* wlo, int k,
+                     int (*on_piece)(void*, int), void* ctx);
+int host_unpack_pieces(const uint32_t* src, int8_t* dst, int64_t nbytes, const int64_t* wlo, int k,
+                       int (*landed)(void*, int), void* ctx);
 int host_pool_threads();
 
 // hga_step_host on a rejected upload: the fitness copy-back returns the uploaded values
@@ -697,6 +699,201 @@ __global__ void k_set_state(int64_t* s, int64_t it, int64_t best, int64_t last_r
     const int64_t v[8] = {it, best, last_restart, 0, 0, 0, run, last};
     if (threadIdx.x < 8) s[threadIdx.x] = v[threadIdx.x];
 }
+
+// ---------------------------------------------------------------- hga_step_host_bits
+constexpr int kStepBitsMaxChunks = 16;
+constexpr size_t kStepBitsTail = 256;  // pinned staging of the 8-value state block after the stream
+
+// Pieces of the population: whole groups of 16 matrices (word aligned in the
+// stream, whole CTA groups of the bit kernels), the last piece to the end.
+struct StepPieces {
+    int k;
+    int64_t mlo[kStepBitsMaxChunks + 1], wlo[kStepBitsMaxChunks + 1];
+    StepPieces(int64_t total, int m, int chunks) {
+        k = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(chunks, kStepBitsMaxChunks), total / 16));
+        for (int i = 0; i <= k; ++i) {
+            mlo[i] = i == k ? total : ((total * i / k) & ~(int64_t)15);
+            wlo[i] = i == k ? (total * m * m + 31) / 32 : mlo[i] * m * m / 32;
+        }
+    }
+};
+
+// The device half of one host-state step after the upload, fixed for given
+// buffers: captured once into a CUDA graph (one launch instead of ~20 API
+// calls per step).  Kernels run on a private stream ks; inside the graph each
+// piece's download depends only on its own stream->bits kernel, so the copies
+// overlap the remaining kernels.
+struct StepBitsGraph {
+    hga_run_args a;
+    uint32_t *host_bits, *dev_bits;
+    int64_t* state_out;
+    int32_t* flag_out;
+    int k;
+    int dev;
+    bool want_graph;
+    cudaStream_t ks = nullptr, side = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    // up[i]: piece i uploaded; down[i]: piece i downloaded; flag; gend: graph done; end; join; cap0/1: capture fork/join
+    cudaEvent_t up[kStepBitsMaxChunks] = {}, down[kStepBitsMaxChunks] = {};
+    cudaEvent_t flag = nullptr, gend = nullptr, end = nullptr, join = nullptr, cap0 = nullptr, cap1 = nullptr;
+};
+
+// the pinned 8-value state block in the tail of the host staging (128-byte aligned)
+static int64_t* step_state_stage(uint32_t* host_bits, int64_t nwords) {
+    return reinterpret_cast<int64_t*>(reinterpret_cast<char*>(host_bits) + (((size_t)nwords * 4 + 127) & ~(size_t)127));
+}
+
+static cudaError_t record(cudaEvent_t ev, cudaStream_t st, bool capturing) {
+    return capturing ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal) : cudaEventRecord(ev, st);
+}
+
+// flag down, generation, new population -> stream -> host piece by piece, state down
+static cudaError_t step_bits_tail(StepBitsGraph* g, bool capturing) {
+    const hga_run_args* a = &g->a;
+    const int m = a->m;
+    const int64_t total = 4 * a->n_pairs;
+    const StepPieces P(total, m, g->k);
+    cudaStream_t ks = g->ks, sd = g->side;
+    int32_t* dflag = &reinterpret_cast<RunWs2*>(a->ws)->host_flag;
+    cudaError_t e = cudaMemcpyAsync(g->flag_out, dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, ks);
+    if (e == cudaSuccess) e = record(g->flag, ks, capturing);
+    if (e != cudaSuccess) return e;
+    hga_run_args r = *a;
+    r.gens_this_call = 1;
+    r.flags |= HGA_RUN_FORCE | kRunHostCheck;  // exactly one generation: the new population is in buffer 1
+    int rc = hga_run_prepare(&r, ks);
+    if (!rc) rc = hga_run(&r, ks);
+    if (rc) return rc >= HGA_E_CUDA_BASE ? (cudaError_t)(rc - HGA_E_CUDA_BASE) : cudaErrorInvalidValue;
+    const int W = words_for(m);
+    for (int i = 0; i < P.k && e == cudaSuccess; ++i) {
+        if (cols_to_bits(a->pop[1] + P.mlo[i] * m * W, P.mlo[i + 1] - P.mlo[i], m, g->dev_bits + P.wlo[i], dflag, ks))
+            return cudaGetLastError();
+        // the download of piece i waits for its own kernel only
+        e = cudaEventRecord(g->cap0, ks);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, g->cap0, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(g->host_bits + P.wlo[i], g->dev_bits + P.wlo[i], (P.wlo[i + 1] - P.wlo[i]) * 4,
+                                cudaMemcpyDeviceToHost, sd);
+        if (e == cudaSuccess) e = record(g->down[i], sd, capturing);
+    }
+    if (e != cudaSuccess) return e;
+    // a rejected population (NOT_GA): the fitness copy-back returns the uploaded values
+    k_fit_restore_if<<<(unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count_cached() * 4), 256, 0, ks>>>(
+        a->fit[0], a->fit[1], total, dflag);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->state_out, a->state, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, ks);
+    if (e == cudaSuccess) e = cudaEventRecord(g->cap1, sd);  // join the download branch back
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ks, g->cap1, 0);
+    return e;  // the fitness goes down outside the graph: the caller's array may not be page-locked
+}
+
+static void step_bits_free(StepBitsGraph* g) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    for (cudaEvent_t ev : g->up)
+        if (ev) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : g->down)
+        if (ev) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : {g->flag, g->gend, g->end, g->join, g->cap0, g->cap1})
+        if (ev) cudaEventDestroy(ev);
+    if (g->ks) cudaStreamDestroy(g->ks);
+    if (g->side) cudaStreamDestroy(g->side);
+    delete g;
+}
+
+// Cached per thread by every input of the device half (buffers, config,
+// seed, piece count, device): a cached graph is exactly the work it stands for.
+static StepBitsGraph* step_bits_graph(const hga_run_args* a, uint32_t* host_bits, uint32_t* dev_bits,
+                                      int64_t* state_out, int32_t* flag_out, int k) {
+    thread_local std::vector<StepBitsGraph*> cache;
+    const int dev = current_device();
+    // HGA_STEP_GRAPH=0 enqueues the same work call by call instead
+    const char* env = std::getenv("HGA_STEP_GRAPH");
+    const bool want_graph = !(env && env[0] == '0');
+    for (size_t i = 0; i < cache.size(); ++i) {
+        StepBitsGraph* g = cache[i];
+        if (g->dev == dev && g->k == k && g->want_graph == want_graph && g->host_bits == host_bits &&
+            g->dev_bits == dev_bits && g->state_out == state_out && g->flag_out == flag_out &&
+            std::memcmp(&g->a, a, sizeof(hga_run_args)) == 0) {
+            if (i) std::swap(cache[i], cache[0]);  // most recent first
+            return g;
+        }
+    }
+    StepBitsGraph* g = new StepBitsGraph();
+    g->a = *a;
+    g->host_bits = host_bits;
+    g->dev_bits = dev_bits;
+    g->state_out = state_out;
+    g->flag_out = flag_out;
+    g->k = k;
+    g->dev = dev;
+    g->want_graph = want_graph;
+    bool ok = cudaStreamCreateWithFlags(&g->ks, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; i < kStepBitsMaxChunks && ok; ++i)
+        ok = cudaEventCreateWithFlags(&g->up[i], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&g->down[i], cudaEventDisableTiming) == cudaSuccess;
+    for (cudaEvent_t* ev : {&g->flag, &g->gend, &g->end, &g->join, &g->cap0, &g->cap1})
+        ok = ok && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        step_bits_free(g);
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (want_graph) {
+        cudaGraph_t graph = nullptr;
+        if (cudaStreamBeginCapture(g->ks, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+            const cudaError_t ce = step_bits_tail(g, true);
+            const cudaError_t ee = cudaStreamEndCapture(g->ks, &graph);
+            cudaError_t ie = cudaErrorUnknown;
+            if (ce == cudaSuccess && ee == cudaSuccess && graph) {
+                ie = cudaGraphInstantiate(&g->exec, graph, 0);
+                if (ie != cudaSuccess) g->exec = nullptr;
+            }
+            if (std::getenv("HGA_STEP_TIMING"))
+                std::fprintf(stderr, "hga_step_host_bits graph capture: enqueue %s, end %s, instantiate %s\n",
+                             cudaGetErrorString(ce), cudaGetErrorString(ee), cudaGetErrorString(ie));
+            if (graph) cudaGraphDestroy(graph);
+        }
+        cudaGetLastError();  // a refused capture leaves the call-by-call path
+    }
+    if (cache.size() >= 8) {
+        step_bits_free(cache.back());
+        cache.pop_back();
+    }
+    cache.insert(cache.begin(), g);
+    return g;
+}
+
+struct StepUpload {  // on_piece context of the host pack
+    StepBitsGraph* g;
+    const StepPieces* P;
+    cudaStream_t cs;
+    int32_t* dflag;
+    cudaError_t e;
+};
+
+// piece i is packed: upload it, then turn it into column records on ks
+static int step_upload_piece(void* ctx, int i) {
+    StepUpload& u = *static_cast<StepUpload*>(ctx);
+    StepBitsGraph* g = u.g;
+    const int m = g->a.m;
+    cudaError_t e = cudaMemcpyAsync(g->dev_bits + u.P->wlo[i], g->host_bits + u.P->wlo[i],
+                                    (u.P->wlo[i + 1] - u.P->wlo[i]) * 4, cudaMemcpyHostToDevice, u.cs);
+    if (e == cudaSuccess) e = cudaEventRecord(g->up[i], u.cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(g->ks, g->up[i], 0);
+    if (e == cudaSuccess &&
+        bits_to_cols(g->dev_bits + u.P->wlo[i], u.P->mlo[i + 1] - u.P->mlo[i], m,
+                     g->a.pop[0] + u.P->mlo[i] * m * words_for(m), u.dflag, g->ks))
+        e = cudaGetLastError();
+    u.e = e;
+    return e == cudaSuccess ? 0 : 1;
+}
+
+static int step_piece_landed(void* ctx, int i) {
+    StepBitsGraph* g = static_cast<StepBitsGraph*>(ctx);
+    return cudaEventSynchronize(g->down[i]) == cudaSuccess ? 0 : 1;
+}
+
 }  // namespace hga
 
 using namespace hga;
@@ -880,112 +1077,79 @@ int hga_step_host(const hga_run_args* a, int8_t* host_pop, int64_t* host_fit, in
 size_t hga_step_host_bits_bytes(int64_t n_pairs, int32_t m) {
     if (n_pairs < 1 || m < 4 || m > 64 || (m & 3)) return 0;
     const int64_t nbytes = 4 * n_pairs * (int64_t)m * m;
-    return (size_t)((nbytes + 31) / 32) * 4;
+    return (size_t)((nbytes + 31) / 32) * 4 + kStepBitsTail;  // + the pinned state block
 }
 
 int hga_step_host_bits(const hga_run_args* a, int8_t* host_pop, int64_t* host_fit, uint32_t* host_bits,
                        uint32_t* dev_bits, const int64_t* state_in, int64_t* state_out, int32_t* flag_out,
                        int32_t chunks, void* stream, void* copy_stream) {
     if (!run_args_ok(a) || !host_pop || !host_fit || !host_bits || !dev_bits || !state_in || !state_out || !flag_out ||
-        chunks < 1)
+        chunks < 1 || !copy_stream)
         return HGA_E_INVALID;
     if (!run2_supported(a) || (a->m & 3)) return HGA_E_UNSUPPORTED;
-    cudaStream_t st = (cudaStream_t)stream, cs = (cudaStream_t)copy_stream;
     const int m = a->m;
     const int64_t total = 4 * a->n_pairs, nbytes = total * (int64_t)m * m, nwords = (nbytes + 31) / 32;
-    const int k = (int)std::min<int64_t>(std::min<int32_t>(chunks, 64), nwords);
-    int32_t* dflag = &reinterpret_cast<RunWs2*>(a->ws)->host_flag;
-    auto wlo = [&](int i) { return nwords * i / k; };
-    thread_local std::vector<cudaEvent_t> pool;  // see hga_step_host
-    while ((int)pool.size() < 2 * k + 4) {
-        cudaEvent_t ne;
-        const cudaError_t ce = cudaEventCreateWithFlags(&ne, cudaEventDisableTiming);
-        if (ce != cudaSuccess) return to_rc(ce);
-        pool.push_back(ne);
-    }
-    cudaEvent_t* ev = pool.data();  // [0..k) pieces copied down, k: buffers free, k+1: upload done, k+2: flag, k+3: end
+    const StepPieces P(total, m, chunks);
     const bool tm = std::getenv("HGA_STEP_TIMING") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
     const auto t0 = now();
+    StepBitsGraph* g = step_bits_graph(a, host_bits, dev_bits, state_out, flag_out, P.k);
+    if (!g) return HGA_E_CUDA_BASE + (int)cudaErrorUnknown;
+    cudaStream_t cs = (cudaStream_t)copy_stream, ks = g->ks;
+    int32_t* dflag = &reinterpret_cast<RunWs2*>(a->ws)->host_flag;
+    // after the work already queued on `stream` (the buffers are free); the
+    // previous call on this staging has completed (its end event was synchronised)
+    cudaError_t e = cudaEventRecord(g->join, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ks, g->join, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, g->join, 0);
     *flag_out = 0;
-    // the device staging and the packed buffers are free once prior work on `stream` is done
-    cudaError_t e = cudaEventRecord(ev[k], st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[k], 0);
+    int64_t* st_stage = step_state_stage(host_bits, nwords);
+    const int64_t sv[8] = {state_in[0], state_in[1], state_in[2], 0, 0, 0, state_in[6], state_in[7]};
+    for (int i = 0; i < 8; ++i) st_stage[i] = sv[i];
+    if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int32_t), ks);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(a->state, st_stage, 8 * sizeof(int64_t), cudaMemcpyHostToDevice, ks);
     if (e == cudaSuccess) e = cudaMemcpyAsync(a->fit[0], host_fit, total * sizeof(int64_t), cudaMemcpyHostToDevice, cs);
     if (e != cudaSuccess) return to_rc(e);
-    // host: validate + pack piece i, then its upload goes out while piece i + 1 is packed
-    int bad = 0;
-    for (int i = 0; i < k && !bad; ++i) {
-        bad = host_pack_bits(host_pop, nbytes, host_bits, wlo(i), wlo(i + 1));
-        if (!bad)
-            e = cudaMemcpyAsync(dev_bits + wlo(i), host_bits + wlo(i), (wlo(i + 1) - wlo(i)) * 4, cudaMemcpyHostToDevice, cs);
-        if (e != cudaSuccess) return to_rc(e);
-    }
+    // host: validate + pack the pieces on the pool; each packed piece is uploaded and turned
+    // into column records while the next ones are still being packed
+    StepUpload up{g, &P, cs, dflag, cudaSuccess};
+    const int prc = host_pack_pieces(host_pop, nbytes, host_bits, P.wlo, P.k, step_upload_piece, &up);
     const auto t1 = now();
-    if (bad) {  // an entry is not +-1: nothing was written to the caller's arrays
+    if (prc) {
         e = cudaStreamSynchronize(cs);
-        *flag_out = HGA_FLAG_NOT_SIGN;
-        return to_rc(e);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ks);
+        if (prc == 1) {  // an entry is not +-1: nothing that could touch the caller's arrays was enqueued
+            *flag_out = HGA_FLAG_NOT_SIGN;
+            return to_rc(e);
+        }
+        return to_rc(up.e != cudaSuccess ? up.e : cudaErrorUnknown);
     }
-    e = cudaEventRecord(ev[k + 1], cs);
-    if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int32_t), st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[k + 1], 0);
-    if (e != cudaSuccess) return to_rc(e);
-    int rc = bits_to_cols(dev_bits, total, m, a->pop[0], dflag, st);
-    if (rc) return rc;
-    e = cudaEventRecord(ev[k + 2], st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[k + 2], 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(flag_out, dflag, sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
-    if (e == cudaSuccess) e = cudaEventRecord(ev[k + 2], cs);
-    if (e != cudaSuccess) return to_rc(e);
-    k_set_state<<<1, 8, 0, st>>>(a->state, state_in[0], state_in[1], state_in[2], state_in[6], state_in[7]);
-    hga_run_args r = *a;
-    r.gens_this_call = 1;
-    r.flags |= HGA_RUN_FORCE | kRunHostCheck;  // exactly one generation: the new population is in buffer 1
-    rc = hga_run_prepare(&r, st);
-    if (!rc) rc = hga_run(&r, st);
-    if (rc) return rc;
-    for (int i = 0; i < k && e == cudaSuccess; ++i) {
-        rc = cols_to_bits(a->pop[1], total, m, wlo(i), wlo(i + 1), dev_bits, dflag, st);
-        if (rc) return rc;
-        e = cudaEventRecord(ev[i], st);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[i], 0);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(host_bits + wlo(i), dev_bits + wlo(i), (wlo(i + 1) - wlo(i)) * 4, cudaMemcpyDeviceToHost, cs);
-        if (e == cudaSuccess) e = cudaEventRecord(ev[i], cs);
-    }
-    if (e == cudaSuccess) {
-        // a rejected population (NOT_GA): the fitness copy-back returns the uploaded values
-        k_fit_restore_if<<<(unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count_cached() * 4), 256, 0,
-                           st>>>(a->fit[0], a->fit[1], total, dflag);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaEventRecord(ev[k + 3], st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev[k + 3], 0);
+    e = g->exec ? cudaGraphLaunch(g->exec, ks) : step_bits_tail(g, false);
+    if (e == cudaSuccess) e = cudaEventRecord(g->gend, ks);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, g->gend, 0);
     if (e == cudaSuccess) e = cudaMemcpyAsync(host_fit, a->fit[1], total * sizeof(int64_t), cudaMemcpyDeviceToHost, cs);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(state_out, a->state, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(g->end, cs);
     if (e != cudaSuccess) return to_rc(e);
     const auto t2 = now();
     // host: the validation flag first (on NOT_GA the caller's population stays as it is), then
-    // unpack each piece as soon as it has landed while the later pieces are still in flight
-    e = cudaEventSynchronize(ev[k + 2]);
+    // unpack each piece on the pool as soon as it has landed while later pieces are in flight
+    e = cudaEventSynchronize(g->flag);
     if (e != cudaSuccess) return to_rc(e);
     const auto t3 = now();
-    if (!(*flag_out & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA))) {
-        for (int i = 0; i < k; ++i) {
-            e = cudaEventSynchronize(ev[i]);
-            if (e != cudaSuccess) return to_rc(e);
-            host_unpack_bits(host_bits, host_pop, nbytes, wlo(i), wlo(i + 1));
-        }
-    }
+    int urc = 0;
+    if (!(*flag_out & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA)))
+        urc = host_unpack_pieces(host_bits, host_pop, nbytes, P.wlo, P.k, step_piece_landed, g);
     const auto t4 = now();
-    e = cudaStreamSynchronize(cs);
+    e = cudaEventSynchronize(g->end);
+    if (e == cudaSuccess && urc) e = cudaErrorUnknown;
     if (tm) {
         auto us = [&](std::chrono::steady_clock::time_point x) {
             return std::chrono::duration<double, std::micro>(x - t0).count();
         };
-        std::fprintf(stderr, "hga_step_host_bits us: packed+uploads_enqueued %.1f enqueued %.1f flag %.1f unpacked %.1f done %.1f (%d host threads)\n",
-                     us(t1), us(t2), us(t3), us(t4), us(now()), host_pool_threads());
+        std::fprintf(stderr,
+                     "hga_step_host_bits us: packed+uploaded %.1f launched %.1f flag %.1f unpacked %.1f done %.1f "
+                     "(%d pieces, %d host threads, graph %d)\n",
+                     us(t1), us(t2), us(t3), us(t4), us(now()), P.k, host_pool_threads(), g->exec != nullptr);
     }
     return to_rc(e);
 }

@@ -36,20 +36,23 @@ class Pool {
         return *p;
     }
     int size() const { return (int)workers_.size() + 1; }
-    // Runs fn(ctx, t) for t in [0, ntasks) on the pool and the calling thread;
-    // returns when all tasks are done.  One job at a time (callers serialise).
-    void run(int ntasks, void (*fn)(void*, int), void* ctx) {
-        std::lock_guard<std::mutex> job_lock(job_mu_);
-        if (workers_.empty() || ntasks <= 1 || ntasks >= (1 << 20)) {
-            for (int t = 0; t < ntasks; ++t) fn(ctx, t);
+    // start(): runs fn(ctx, t) for t in [0, ntasks) on the worker threads; the
+    // calling thread does not take tasks (it drives the CUDA side meanwhile).
+    // wait() returns when all tasks are done.  One job at a time: the job lock
+    // is held from start() to wait().  A worker only takes a task of the job it
+    // sees (compare-exchange on job id | ntasks | next task), so a straggler of
+    // the previous job can never run or count a task of this one.
+    void start(int ntasks, void (*fn)(void*, int), void* ctx) {
+        job_mu_.lock();
+        started_ = ntasks;
+        if (workers_.empty() || ntasks >= (1 << 20)) {
+            for (int t = 0; t < ntasks; ++t) fn(ctx, t);  // no workers: run inline (callbacks still see progress)
+            started_ = -1;
             return;
         }
         fn_ = fn;
         ctx_ = ctx;
         done_.store(0, std::memory_order_relaxed);
-        // ticket = job id | ntasks | next task: a worker only takes a task
-        // of the job it sees (compare-exchange), so a straggler of the
-        // previous job can never run or count a task of this one
         job_ = (job_ + 1) & 0xFFFFFFull;
         ticket_.store((job_ << 40) | ((uint64_t)ntasks << 20), std::memory_order_release);
         {
@@ -57,11 +60,16 @@ class Pool {
             gen_.fetch_add(1, std::memory_order_release);
         }
         cv_.notify_all();
-        work();
-        while (done_.load(std::memory_order_acquire) < ntasks) _mm_pause();
     }
+    void wait() {
+        if (started_ >= 0)
+            while (done_.load(std::memory_order_acquire) < started_) _mm_pause();
+        job_mu_.unlock();
+    }
+    bool inline_mode() const { return workers_.empty(); }
 
    private:
+    int started_ = 0;
     Pool() {
         int n = 0;
         cpu_set_t set;
@@ -181,62 +189,122 @@ static void unpack_scalar(const uint32_t* src, int8_t* dst, int64_t nbytes, int6
         for (int b = 0; b < 32 && 32 * w + b < nbytes; ++b) dst[32 * w + b] = ((src[w] >> b) & 1u) ? -1 : 1;
 }
 
-struct Job {
-    const int8_t* src8;
-    int8_t* dst8;
-    const uint32_t* src32;
-    uint32_t* dst32;
-    int64_t nbytes, w0, w1;
-    int parts;
-    std::atomic<uint32_t> bad{0};
-};
-
-static void pack_task(void* p, int t) {
-    Job& j = *static_cast<Job*>(p);
-    const int64_t n = j.w1 - j.w0, a = j.w0 + n * t / j.parts, b = j.w0 + n * (t + 1) / j.parts;
-    const uint32_t bad = have_avx2() ? pack_avx2(j.src8, j.nbytes, j.dst32, a, b) : pack_scalar(j.src8, j.nbytes, j.dst32, a, b);
-    if (bad) j.bad.fetch_or(1u, std::memory_order_relaxed);
-}
-
-static void unpack_task(void* p, int t) {
-    Job& j = *static_cast<Job*>(p);
-    const int64_t n = j.w1 - j.w0, a = j.w0 + n * t / j.parts, b = j.w0 + n * (t + 1) / j.parts;
-    if (have_avx2()) unpack_avx2(j.src32, j.dst8, j.nbytes, a, b);
-    else unpack_scalar(j.src32, j.dst8, j.nbytes, a, b);
-}
-
 static int parts_for(int64_t words) {
     // ~16 KB of int8 per task at least: dispatch costs ~1 us per task
     const int64_t p = std::max<int64_t>(1, words / 512);
     return (int)std::min<int64_t>(p, 4 * (int64_t)Pool::get().size());
 }
 
+constexpr int kMaxPieces = 64;
+
+// k pieces x `parts` tasks, piece-major, so pieces complete roughly in order
+struct PieceJob {
+    const int8_t* src8 = nullptr;
+    int8_t* dst8 = nullptr;
+    const uint32_t* src32 = nullptr;
+    uint32_t* dst32 = nullptr;
+    int64_t nbytes = 0;
+    const int64_t* wlo = nullptr;
+    int k = 0, parts = 1;
+    std::atomic<int> piece_done[kMaxPieces];
+    std::atomic<int> ready[kMaxPieces];
+    std::atomic<int> abort{0};
+    std::atomic<uint32_t> bad{0};
+    PieceJob() {
+        for (auto& x : piece_done) x.store(0, std::memory_order_relaxed);
+        for (auto& x : ready) x.store(0, std::memory_order_relaxed);
+    }
+    void range(int t, int64_t& a, int64_t& b) const {
+        const int i = t / parts, q = t % parts;
+        const int64_t n = wlo[i + 1] - wlo[i];
+        a = wlo[i] + n * q / parts;
+        b = wlo[i] + n * (q + 1) / parts;
+    }
+};
+
+static void pack_piece_task(void* p, int t) {
+    PieceJob& j = *static_cast<PieceJob*>(p);
+    int64_t a, b;
+    j.range(t, a, b);
+    const uint32_t bad = have_avx2() ? pack_avx2(j.src8, j.nbytes, j.dst32, a, b) : pack_scalar(j.src8, j.nbytes, j.dst32, a, b);
+    if (bad) j.bad.fetch_or(1u, std::memory_order_relaxed);
+    j.piece_done[t / j.parts].fetch_add(1, std::memory_order_release);
+}
+
+static void unpack_piece_task(void* p, int t) {
+    PieceJob& j = *static_cast<PieceJob*>(p);
+    const int i = t / j.parts;
+    while (!j.ready[i].load(std::memory_order_acquire)) _mm_pause();  // the piece has landed
+    if (j.abort.load(std::memory_order_relaxed)) return;
+    int64_t a, b;
+    j.range(t, a, b);
+    if (have_avx2()) unpack_avx2(j.src32, j.dst8, j.nbytes, a, b);
+    else unpack_scalar(j.src32, j.dst8, j.nbytes, a, b);
+}
+
 }  // namespace host
 
-// Pack bytes of words [w0, w1): returns 1 when some byte is not +-1.
-int host_pack_bits(const int8_t* src, int64_t nbytes, uint32_t* dst, int64_t w0, int64_t w1) {
-    if (w1 <= w0) return 0;
-    host::Job j;
+// Pack the stream words [wlo[0], wlo[k]) in k pieces on the pool; on_piece(ctx, i)
+// runs on the calling thread as soon as piece i is packed (in order; stops
+// being called after a nonzero return, which is passed back).  Returns 1 when some
+// byte is not +-1 (no more pieces are handed out then), else on_piece's status.
+int host_pack_pieces(const int8_t* src, int64_t nbytes, uint32_t* dst, const int64_t* wlo, int k,
+                     int (*on_piece)(void*, int), void* ctx) {
+    if (k < 1 || k > host::kMaxPieces) return -1;
+    host::Pool& pool = host::Pool::get();
+    host::PieceJob j;
     j.src8 = src;
     j.dst32 = dst;
     j.nbytes = nbytes;
-    j.w0 = w0;
-    j.w1 = w1;
-    j.parts = host::parts_for(w1 - w0);
-    host::Pool::get().run(j.parts, host::pack_task, &j);
-    return j.bad.load() ? 1 : 0;
+    j.wlo = wlo;
+    j.k = k;
+    j.parts = std::max(1, host::parts_for((wlo[k] - wlo[0]) / k));
+    pool.start(k * j.parts, host::pack_piece_task, &j);
+    int rc = 0;
+    for (int i = 0; i < k && !rc; ++i) {
+        while (j.piece_done[i].load(std::memory_order_acquire) < j.parts) _mm_pause();
+        if (j.bad.load(std::memory_order_relaxed)) break;
+        rc = on_piece(ctx, i);
+    }
+    pool.wait();
+    return j.bad.load() ? 1 : rc;
 }
 
-void host_unpack_bits(const uint32_t* src, int8_t* dst, int64_t nbytes, int64_t w0, int64_t w1) {
-    if (w1 <= w0) return;
-    host::Job j;
+// Unpack the stream words [wlo[0], wlo[k]) in k pieces on the pool: piece i is
+// unpacked as soon as landed(ctx, i) -- called on the calling thread, in
+// order -- has returned 0; a nonzero return skips the remaining pieces.
+int host_unpack_pieces(const uint32_t* src, int8_t* dst, int64_t nbytes, const int64_t* wlo, int k,
+                       int (*landed)(void*, int), void* ctx) {
+    if (k < 1 || k > host::kMaxPieces) return -1;
+    host::Pool& pool = host::Pool::get();
+    host::PieceJob j;
     j.src32 = src;
     j.dst8 = dst;
     j.nbytes = nbytes;
-    j.w0 = w0;
-    j.w1 = w1;
-    j.parts = host::parts_for(w1 - w0);
-    host::Pool::get().run(j.parts, host::unpack_task, &j);
+    j.wlo = wlo;
+    j.k = k;
+    j.parts = std::max(1, host::parts_for((wlo[k] - wlo[0]) / k));
+    if (pool.inline_mode()) {  // no workers: wait, then unpack inline
+        int rc = 0;
+        for (int i = 0; i < k && !rc; ++i) {
+            rc = landed(ctx, i);
+            if (!rc)
+                for (int q = 0; q < j.parts; ++q) {
+                    j.ready[i].store(1);
+                    host::unpack_piece_task(&j, i * j.parts + q);
+                }
+        }
+        return rc;
+    }
+    pool.start(k * j.parts, host::unpack_piece_task, &j);
+    int rc = 0;
+    for (int i = 0; i < k; ++i) {
+        if (!rc) rc = landed(ctx, i);
+        if (rc) j.abort.store(1, std::memory_order_relaxed);
+        j.ready[i].store(1, std::memory_order_release);
+    }
+    pool.wait();
+    return rc;
 }
 
 int host_pool_threads() { return host::Pool::get().size(); }

@@ -872,35 +872,62 @@ class _HostBridge:
         return self._bits or None
 
     def pin(self, arr: np.ndarray) -> None:
-        """Page-lock `arr` in place; not fatal when the runtime refuses (already
-        pinned or registered memory, overlapping ranges): the copies then go
-        through the driver's staging path and the error state is cleared."""
+        """Page-lock `arr` in place (shared, reference-counted registration,
+        see _pin); not fatal when the runtime refuses (already pinned memory):
+        the copies then go through the driver's staging path."""
         addr = arr.ctypes.data
         held = self.registered.get(addr)
         if arr.nbytes == 0 or (held is not None and held.nbytes >= arr.nbytes):
             return
-        try:
-            rt = torch.cuda.cudart()
-            if held is not None:  # same address, larger array: re-register the whole range
-                rt.cudaHostUnregister(addr)
-                del self.registered[addr]
-            rc = int(rt.cudaHostRegister(addr, arr.nbytes, 0))
-        except Exception:  # noqa: BLE001 -- registration is an optimisation only
-            rc = -1
-        if rc == 0:
+        if held is not None:
+            _unpin(addr)
+            del self.registered[addr]
+        if _pin(arr):
             self.registered[addr] = arr
-        else:
+
+
+# Page-locked host ranges, shared by every bridge: address -> [array, users].
+# Two host states over the same arrays (or a new state reusing a freed
+# state's address) share one registration; it is dropped with its last user.
+_PINNED: dict[int, list] = {}
+
+
+def _pin(arr: np.ndarray) -> bool:
+    addr = arr.ctypes.data
+    ent = _PINNED.get(addr)
+    if ent is not None:
+        if ent[0].nbytes >= arr.nbytes:
+            ent[1] += 1
+            return True
+        return False  # a smaller live registration at this address: use staged copies
+    try:
+        rc = int(torch.cuda.cudart().cudaHostRegister(addr, arr.nbytes, 0))
+    except Exception:  # noqa: BLE001 -- registration is an optimisation only
+        rc = -1
+    if rc != 0:
+        lib.hga_clear_last_error()
+        return False
+    _PINNED[addr] = [arr, 1]
+    return True
+
+
+def _unpin(addr: int) -> None:
+    ent = _PINNED.get(addr)
+    if ent is None:
+        return
+    ent[1] -= 1
+    if ent[1] <= 0:
+        del _PINNED[addr]
+        try:
+            torch.cuda.cudart().cudaHostUnregister(addr)
             lib.hga_clear_last_error()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
 
 
 def _unregister_all(registered: dict) -> None:
-    try:
-        rt = torch.cuda.cudart()
-        for addr in list(registered):
-            rt.cudaHostUnregister(addr)
-        lib.hga_clear_last_error()
-    except Exception:  # noqa: BLE001 -- interpreter shutdown
-        pass
+    for addr in list(registered):
+        _unpin(addr)
     registered.clear()
 
 
@@ -958,7 +985,8 @@ def _step_host(state):
     """
     bridge = _bridge_for(state)
     pop_np, fit_np = _host_arrays(state, bridge.cfg)
-    bridge.pin(pop_np)
+    if bridge.bit_buffers() is None:  # the bit-stream path reads / writes the population with the host's cores
+        bridge.pin(pop_np)
     bridge.pin(fit_np)
     res = bridge.res
     res.cur = 0  # the host arrays are authoritative: upload into buffer 0

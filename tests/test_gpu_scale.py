@@ -432,7 +432,7 @@ def test_orders_above_128_run_the_reference_generation(m, N, fit, mut, cuda_devi
 # ------------------------------------------------------------ bit-stream host step
 
 
-@pytest.mark.parametrize("m,N,fit,nc,nr", [(4, 3, "f1", 1, 1), (20, 10_000, "f2", 4, 2), (36, 500, "f2", 1, 12),
+@pytest.mark.parametrize("m,N,fit,nc,nr", [(4, 3, "f1", 1, 1), (16, 77, "f2", 1, 1), (20, 10_000, "f2", 4, 2), (36, 500, "f2", 1, 12),
                                            (48, 257, "f1", 2, 3), (64, 300, "f2", 3, 5), (12, 40, "sq", 2, 2),
                                            (36, 64, "sq", 2, 2)])
 def test_host_step_bit_stream_matches_byte_path(m, N, fit, nc, nr, cuda_device, monkeypatch):
