@@ -101,6 +101,12 @@ __global__ void __launch_bounds__(128, 1) k_probe_mma_i8(int64_t iters, uint32_t
     }
 }
 
+// launch-cost probe: every thread touches one word (so the CTA really runs)
+__global__ void k_probe_empty(uint32_t* out) {
+    extern __shared__ uint32_t sm_dummy[];
+    if (threadIdx.x == 0 && blockIdx.x == 0 && out) out[0] = sm_dummy[0] & 0u;
+}
+
 }  // namespace hga
 
 extern "C" int hga_probe(int32_t kind, int64_t iters, int32_t blocks, int32_t threads, uint32_t* out,
@@ -131,6 +137,17 @@ extern "C" int hga_probe(int32_t kind, int64_t iters, int32_t blocks, int32_t th
         if (e != cudaSuccess) return hga::to_rc(e);
         void* args[] = {(void*)&iters, (void*)&out};
         e = cudaLaunchKernel(k, dim3(blocks), dim3(128), args, smem, st);
+        if (e != cudaSuccess) return hga::to_rc(e);
+    } else if (kind == 10 || kind == 11) {
+        // launch cost of a kernel shaped like the generation loop: `blocks` CTAs of
+        // `threads` threads with `iters` bytes of dynamic shared memory; 10 = plain
+        // launch, 11 = cooperative launch
+        const int smem = (int)iters;
+        cudaError_t e = cudaFuncSetAttribute((void*)hga::k_probe_empty, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return hga::to_rc(e);
+        void* args[] = {(void*)&out};
+        e = kind == 10 ? cudaLaunchKernel((void*)hga::k_probe_empty, dim3(blocks), dim3(threads), args, smem, st)
+                       : cudaLaunchCooperativeKernel((void*)hga::k_probe_empty, dim3(blocks), dim3(threads), args, smem, st);
         if (e != cudaSuccess) return hga::to_rc(e);
     } else {
         return HGA_E_INVALID;

@@ -971,6 +971,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     TileSharedTP* T1 = reinterpret_cast<TileSharedTP*>(gbase + 2 * kRowsBytes + kTPS);
     int8_t* tplan = reinterpret_cast<int8_t*>(gbase + 2 * kRowsBytes + 2 * kTPS);
 
+    if ((A.flags & HGA_RUN_TIMING) && bid == 0 && tid == 0) ws->tstamp[63][0] = gtimer();  // kernel entry
     if ((A.flags & kRunHostCheck) && (__ldcg(&ws->host_flag) & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA)))
         return;  // uniform over the grid: no barrier has been entered
     int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
@@ -1374,6 +1375,7 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
         A.state[5] = (best == 0 || iter >= A.max_generation) ? 1 : 0;
         A.state[6] = run;
         A.state[7] = last_val;
+        if (A.flags & HGA_RUN_TIMING) ws->tstamp[63][1] = gtimer();  // CTA 0 done
     }
 }
 
