@@ -736,6 +736,7 @@ struct StepBitsGraph {
     // up[i]: piece i uploaded; down[i]: piece i downloaded; flag; gend: graph done; end; join; cap0/1: capture fork/join
     cudaEvent_t up[kStepBitsMaxChunks] = {}, down[kStepBitsMaxChunks] = {};
     cudaEvent_t flag = nullptr, gend = nullptr, end = nullptr, join = nullptr, cap0 = nullptr, cap1 = nullptr;
+    cudaEvent_t fitup = nullptr;  // the fitness is uploaded
 };
 
 // the pinned 8-value state block in the tail of the host staging (128-byte aligned)
@@ -761,8 +762,7 @@ static cudaError_t step_bits_tail(StepBitsGraph* g, bool capturing) {
     hga_run_args r = *a;
     r.gens_this_call = 1;
     r.flags |= HGA_RUN_FORCE | kRunHostCheck;  // exactly one generation: the new population is in buffer 1
-    int rc = hga_run_prepare(&r, ks);
-    if (!rc) rc = hga_run(&r, ks);
+    const int rc = hga_run(&r, ks);  // (its select histogram was rebuilt during the upload)
     if (rc) return rc >= HGA_E_CUDA_BASE ? (cudaError_t)(rc - HGA_E_CUDA_BASE) : cudaErrorInvalidValue;
     const int W = words_for(m);
     for (int i = 0; i < P.k && e == cudaSuccess; ++i) {
@@ -793,7 +793,7 @@ static void step_bits_free(StepBitsGraph* g) {
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : g->down)
         if (ev) cudaEventDestroy(ev);
-    for (cudaEvent_t ev : {g->flag, g->gend, g->end, g->join, g->cap0, g->cap1})
+    for (cudaEvent_t ev : {g->flag, g->gend, g->end, g->join, g->cap0, g->cap1, g->fitup})
         if (ev) cudaEventDestroy(ev);
     if (g->ks) cudaStreamDestroy(g->ks);
     if (g->side) cudaStreamDestroy(g->side);
@@ -832,7 +832,7 @@ static StepBitsGraph* step_bits_graph(const hga_run_args* a, uint32_t* host_bits
     for (int i = 0; i < kStepBitsMaxChunks && ok; ++i)
         ok = cudaEventCreateWithFlags(&g->up[i], cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&g->down[i], cudaEventDisableTiming) == cudaSuccess;
-    for (cudaEvent_t* ev : {&g->flag, &g->gend, &g->end, &g->join, &g->cap0, &g->cap1})
+    for (cudaEvent_t* ev : {&g->flag, &g->gend, &g->end, &g->join, &g->cap0, &g->cap1, &g->fitup})
         ok = ok && cudaEventCreateWithFlags(ev, cudaEventDisableTiming) == cudaSuccess;
     if (!ok) {
         step_bits_free(g);
@@ -1109,7 +1109,16 @@ int hga_step_host_bits(const hga_run_args* a, int8_t* host_pop, int64_t* host_fi
     if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int32_t), ks);
     if (e == cudaSuccess) e = cudaMemcpyAsync(a->state, st_stage, 8 * sizeof(int64_t), cudaMemcpyHostToDevice, ks);
     if (e == cudaSuccess) e = cudaMemcpyAsync(a->fit[0], host_fit, total * sizeof(int64_t), cudaMemcpyHostToDevice, cs);
+    // the select histogram of the uploaded fitness is rebuilt while the population is packed
+    if (e == cudaSuccess) e = cudaEventRecord(g->fitup, cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ks, g->fitup, 0);
     if (e != cudaSuccess) return to_rc(e);
+    {
+        hga_run_args r = *a;
+        r.flags |= HGA_RUN_FORCE | kRunHostCheck;
+        const int rc = hga_run_prepare(&r, ks);
+        if (rc) return rc;
+    }
     // host: validate + pack the pieces on the pool; each packed piece is uploaded and turned
     // into column records while the next ones are still being packed
     StepUpload up{g, &P, cs, dflag, cudaSuccess};
