@@ -974,14 +974,6 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
     if ((A.flags & HGA_RUN_TIMING) && bid == 0 && tid == 0) ws->tstamp[63][0] = gtimer();  // kernel entry
     if ((A.flags & kRunHostCheck) && (__ldcg(&ws->host_flag) & (HGA_FLAG_NOT_SIGN | HGA_FLAG_NOT_GA)))
         return;  // uniform over the grid: no barrier has been entered
-    // the select key ranges of all slots, loaded with the state block (one round trip
-    // instead of two before the first generation's threshold scan)
-    uint32_t kmin_pre[3], kmax_pre[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        kmin_pre[q] = __ldcg(&ws->kmin[q]);
-        kmax_pre[q] = __ldcg(&ws->kmax[q]);
-    }
     int64_t iter = A.state[0], best = A.state[1], last_restart = A.state[2];
     int parity = (int)A.state[3];
     if (A.flags & (kRunPrefetchPop | kRunPrefetchFit)) {
@@ -1045,8 +1037,8 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
                                  : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
             }
             if (!have_krange) {
-                next_kmin = gi == 0 ? kmin_pre[rslot] : __ldcg(&ws->kmin[rslot]);
-                next_kmax = gi == 0 ? kmax_pre[rslot] : __ldcg(&ws->kmax[rslot]);
+                next_kmin = __ldcg(&ws->kmin[rslot]);
+                next_kmax = __ldcg(&ws->kmax[rslot]);
             }
             kmin = next_kmin;
             kmax = next_kmax;
@@ -1096,8 +1088,8 @@ __global__ void __launch_bounds__(kR2Threads* GROUPS, 1) k_run_v3(Run2Params P) 
             if (!have_fpre && wid < pw_sel) load_items(f_old, lo + (int64_t)tid * kSelItems, hi, fpre);
             have_fpre = false;
             if (!have_krange) {  // otherwise read with the bookkeeping loads of the previous generation
-                next_kmin = gi == 0 ? kmin_pre[rslot] : __ldcg(&ws->kmin[rslot]);
-                next_kmax = gi == 0 ? kmax_pre[rslot] : __ldcg(&ws->kmax[rslot]);
+                next_kmin = __ldcg(&ws->kmin[rslot]);
+                next_kmax = __ldcg(&ws->kmax[rslot]);
             }
             kmin = next_kmin;
             kmax = next_kmax;
