@@ -9,10 +9,15 @@
  * Conventions
  *   - extern "C", plain pointers and sizes, no torch types.
  *   - Every pointer named *pop, *cols, *fit, *out, ... is a DEVICE pointer
- *     (cudaMalloc / torch tensor .data_ptr()).  The library never allocates;
- *     scratch is passed in after a *_ws_bytes query.
+ *     (cudaMalloc / torch tensor .data_ptr()).  The library never allocates
+ *     device or pinned memory; scratch is passed in after a *_ws_bytes query.
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
- *     asynchronous on that stream and never synchronize the host.
+ *     asynchronous on that stream and never synchronize the host -- except
+ *     the host-state steps (hga_step_host*), which return with the caller's
+ *     host arrays updated.  hga_step_host_bits keeps, per calling thread, a
+ *     small cache of CUDA graphs / private streams / events keyed by its
+ *     buffers, and uses one process-wide host thread pool (calls from
+ *     several threads are serialised on it).
  *   - Return 0 (HGA_OK) or an error code; argument errors are detected on the
  *     host before any launch.  Data-dependent errors (a point or plan index
  *     out of range, an entry that is not +-1) are reported through an optional

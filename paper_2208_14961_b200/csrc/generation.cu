@@ -680,7 +680,7 @@ int unpack_i8_guarded(const uint32_t* cols, int64_t n, int32_t m, int8_t* pop, c
 int bits_to_cols(const uint32_t* bits, int64_t n, int32_t m, uint32_t* cols, int32_t* flag, cudaStream_t st);
 int cols_to_bits(const uint32_t* cols, int64_t n, int32_t m, uint32_t* bits, const int32_t* skip, cudaStream_t st);
 int host_pack_pieces(const int8_t* src, int64_t nbytes, uint32_t* dst, const int64_t* wlo, int k,
-                     int (*on_piece)(void*, int), void* ctx);
+                     int (*started)(void*), int (*on_piece)(void*, int), void* ctx);
 int host_unpack_pieces(const uint32_t* src, int8_t* dst, int64_t nbytes, const int64_t* wlo, int k,
                        int (*landed)(void*, int), void* ctx);
 int host_pool_threads();
@@ -864,13 +864,40 @@ static StepBitsGraph* step_bits_graph(const hga_run_args* a, uint32_t* host_bits
     return g;
 }
 
-struct StepUpload {  // on_piece context of the host pack
+struct StepUpload {  // callback context of the host pack
     StepBitsGraph* g;
     const StepPieces* P;
-    cudaStream_t cs;
+    cudaStream_t cs, user;
     int32_t* dflag;
+    const int64_t* host_fit;
+    const int64_t* st_stage;
     cudaError_t e;
 };
+
+// while the workers pack: join the caller's stream, reset the flag, state and
+// fitness up, and the select histogram of the uploaded fitness rebuilt
+static int step_upload_started(void* ctx) {
+    StepUpload& u = *static_cast<StepUpload*>(ctx);
+    StepBitsGraph* g = u.g;
+    const hga_run_args* a = &g->a;
+    const int64_t total = 4 * a->n_pairs;
+    cudaError_t e = cudaEventRecord(g->join, u.user);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(g->ks, g->join, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(u.cs, g->join, 0);
+    if (e == cudaSuccess) e = cudaMemsetAsync(u.dflag, 0, sizeof(int32_t), g->ks);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(a->state, u.st_stage, 8 * sizeof(int64_t), cudaMemcpyHostToDevice, g->ks);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(a->fit[0], u.host_fit, total * sizeof(int64_t), cudaMemcpyHostToDevice, u.cs);
+    if (e == cudaSuccess) e = cudaEventRecord(g->fitup, u.cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(g->ks, g->fitup, 0);
+    if (e == cudaSuccess) {
+        hga_run_args r = *a;
+        r.flags |= HGA_RUN_FORCE | kRunHostCheck;
+        const int rc = hga_run_prepare(&r, g->ks);
+        if (rc) e = rc >= HGA_E_CUDA_BASE ? (cudaError_t)(rc - HGA_E_CUDA_BASE) : cudaErrorInvalidValue;
+    }
+    u.e = e;
+    return e == cudaSuccess ? 0 : 1;
+}
 
 // piece i is packed: upload it, then turn it into column records on ks
 static int step_upload_piece(void* ctx, int i) {
@@ -1097,32 +1124,18 @@ int hga_step_host_bits(const hga_run_args* a, int8_t* host_pop, int64_t* host_fi
     if (!g) return HGA_E_CUDA_BASE + (int)cudaErrorUnknown;
     cudaStream_t cs = (cudaStream_t)copy_stream, ks = g->ks;
     int32_t* dflag = &reinterpret_cast<RunWs2*>(a->ws)->host_flag;
-    // after the work already queued on `stream` (the buffers are free); the
-    // previous call on this staging has completed (its end event was synchronised)
-    cudaError_t e = cudaEventRecord(g->join, (cudaStream_t)stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ks, g->join, 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, g->join, 0);
+    // the previous call on this staging has completed (its end event was synchronised)
     *flag_out = 0;
     int64_t* st_stage = step_state_stage(host_bits, nwords);
     const int64_t sv[8] = {state_in[0], state_in[1], state_in[2], 0, 0, 0, state_in[6], state_in[7]};
     for (int i = 0; i < 8; ++i) st_stage[i] = sv[i];
-    if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int32_t), ks);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(a->state, st_stage, 8 * sizeof(int64_t), cudaMemcpyHostToDevice, ks);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(a->fit[0], host_fit, total * sizeof(int64_t), cudaMemcpyHostToDevice, cs);
-    // the select histogram of the uploaded fitness is rebuilt while the population is packed
-    if (e == cudaSuccess) e = cudaEventRecord(g->fitup, cs);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ks, g->fitup, 0);
-    if (e != cudaSuccess) return to_rc(e);
-    {
-        hga_run_args r = *a;
-        r.flags |= HGA_RUN_FORCE | kRunHostCheck;
-        const int rc = hga_run_prepare(&r, ks);
-        if (rc) return rc;
-    }
-    // host: validate + pack the pieces on the pool; each packed piece is uploaded and turned
-    // into column records while the next ones are still being packed
-    StepUpload up{g, &P, cs, dflag, cudaSuccess};
-    const int prc = host_pack_pieces(host_pop, nbytes, host_bits, P.wlo, P.k, step_upload_piece, &up);
+    // host: validate + pack the pieces on the pool; meanwhile this thread queues the
+    // device work that does not need the population (after the work already queued
+    // on `stream`), then uploads each packed piece and turns it into column records
+    // while the next ones are still being packed
+    StepUpload up{g, &P, cs, (cudaStream_t)stream, dflag, host_fit, st_stage, cudaSuccess};
+    const int prc = host_pack_pieces(host_pop, nbytes, host_bits, P.wlo, P.k, step_upload_started, step_upload_piece, &up);
+    cudaError_t e = cudaSuccess;
     const auto t1 = now();
     if (prc) {
         e = cudaStreamSynchronize(cs);

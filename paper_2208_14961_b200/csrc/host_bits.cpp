@@ -244,12 +244,13 @@ static void unpack_piece_task(void* p, int t) {
 
 }  // namespace host
 
-// Pack the stream words [wlo[0], wlo[k]) in k pieces on the pool; on_piece(ctx, i)
-// runs on the calling thread as soon as piece i is packed (in order; stops
-// being called after a nonzero return, which is passed back).  Returns 1 when some
-// byte is not +-1 (no more pieces are handed out then), else on_piece's status.
+// Pack the stream words [wlo[0], wlo[k]) in k pieces on the pool; started(ctx)
+// (optional) runs on the calling thread while the workers pack, then
+// on_piece(ctx, i) as soon as piece i is packed (in order; a nonzero return
+// of either stops the calls and is passed back).  Returns 1 when some byte is
+// not +-1 (no more pieces are handed out then), else the callbacks' status.
 int host_pack_pieces(const int8_t* src, int64_t nbytes, uint32_t* dst, const int64_t* wlo, int k,
-                     int (*on_piece)(void*, int), void* ctx) {
+                     int (*started)(void*), int (*on_piece)(void*, int), void* ctx) {
     if (k < 1 || k > host::kMaxPieces) return -1;
     host::Pool& pool = host::Pool::get();
     host::PieceJob j;
@@ -260,7 +261,7 @@ int host_pack_pieces(const int8_t* src, int64_t nbytes, uint32_t* dst, const int
     j.k = k;
     j.parts = std::max(1, host::parts_for((wlo[k] - wlo[0]) / k));
     pool.start(k * j.parts, host::pack_piece_task, &j);
-    int rc = 0;
+    int rc = started ? started(ctx) : 0;
     for (int i = 0; i < k && !rc; ++i) {
         while (j.piece_done[i].load(std::memory_order_acquire) < j.parts) _mm_pause();
         if (j.bad.load(std::memory_order_relaxed)) break;

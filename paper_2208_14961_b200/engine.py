@@ -985,14 +985,14 @@ def _step_host(state):
     """
     bridge = _bridge_for(state)
     pop_np, fit_np = _host_arrays(state, bridge.cfg)
-    if bridge.bit_buffers() is None:  # the bit-stream path reads / writes the population with the host's cores
-        bridge.pin(pop_np)
-    bridge.pin(fit_np)
     res = bridge.res
     res.cur = 0  # the host arrays are authoritative: upload into buffer 0
     it0, best0 = int(state.iteration), int(state.best_fitness)
     last0 = int(state.trace[-1]) if state.trace else best0
     explicit = bridge.cfg.rng != "philox"
+    if explicit or res.m > 64 or bridge.bit_buffers() is None:
+        bridge.pin(pop_np)  # DMA copies of the int8 population (the bit-stream path packs it on the host instead)
+    bridge.pin(fit_np)
     if not explicit and res.m <= 64:
         # the whole step is enqueued natively (hga_step_host): chunked copies on a
         # side stream overlapped with pack / unpack, one synchronisation at the end
