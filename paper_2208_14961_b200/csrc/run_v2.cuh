@@ -23,6 +23,8 @@
 //   F  bookkeeping replicated in every CTA (trace, best, stop, stall restart)
 #pragma once
 
+#include <cstdlib>
+
 #include "run_common.cuh"
 #include "tile.cuh"
 
@@ -1435,7 +1437,12 @@ int launch_run_v2_k(const hga_run_args* a, cudaStream_t st) {
     }
     const int per_sm = per_sm_dev[dev];
     if (per_sm < 1) return HGA_E_UNSUPPORTED;
-    const int grid = std::min(std::min(sm_count_cached() * std::min(per_sm, 2), kMaxNb), GROUPS * kR2Threads);
+    int grid = std::min(std::min(sm_count_cached() * std::min(per_sm, 2), kMaxNb), GROUPS * kR2Threads);
+    static const int grid_cap = [] {  // HGA_RUN_GRID=<ctas>: experiment, cap the loop's grid (results identical)
+        const char* e = std::getenv("HGA_RUN_GRID");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (grid_cap > 0) grid = std::min(grid, grid_cap);
     void* params[] = {&P};
     if (a->flags & kRunPlainLaunch)  // experiment: ordinary launch (co-residency by construction: grid <= resident CTAs)
         return to_rc(cudaLaunchKernel((const void*)kern, dim3(grid), dim3(kR2Threads * GROUPS), params, smem, st));
