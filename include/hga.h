@@ -296,6 +296,15 @@ int hga_step_host(const hga_run_args *args, int8_t *host_pop, int64_t *host_fit,
  * A byte that is not +-1 returns with *flag_out = HGA_FLAG_NOT_SIGN before
  * any device work that could touch the caller's arrays; HGA_FLAG_NOT_GA
  * leaves host_pop as it was and host_fit holding its own values. */
+/* The host half of hga_step_host_bits as plain host utilities (no GPU):
+ * hga_host_pack_bits packs n int8 entries into ceil(n/32) uint32 words of
+ * the bit stream (bit e % 32 of word e / 32 set iff src[e] == -1; unused
+ * high bits of the last word 0) on libhga's host thread pool and returns
+ * HGA_FLAG_NOT_SIGN when some entry is not +-1 (the words are then
+ * unspecified), else 0; hga_host_unpack_bits writes n entries of +1 / -1
+ * from the stream. */
+int hga_host_pack_bits(const int8_t *src, int64_t n, uint32_t *dst);
+void hga_host_unpack_bits(const uint32_t *src, int64_t n, int8_t *dst);
 size_t hga_step_host_bits_bytes(int64_t n_pairs, int32_t m);
 int hga_step_host_bits(const hga_run_args *args, int8_t *host_pop, int64_t *host_fit, uint32_t *host_bits,
                        uint32_t *dev_bits, const int64_t *state_in, int64_t *state_out, int32_t *flag_out,

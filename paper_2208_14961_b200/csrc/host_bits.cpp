@@ -25,6 +25,8 @@
 #include <thread>
 #include <vector>
 
+#include "../../include/hga.h"
+
 namespace hga {
 namespace host {
 
@@ -311,3 +313,17 @@ int host_unpack_pieces(const uint32_t* src, int8_t* dst, int64_t nbytes, const i
 int host_pool_threads() { return host::Pool::get().size(); }
 
 }  // namespace hga
+
+static int no_piece_cb(void*, int) { return 0; }
+
+extern "C" int hga_host_pack_bits(const int8_t* src, int64_t n, uint32_t* dst) {
+    if (n <= 0) return 0;
+    const int64_t wlo[2] = {0, (n + 31) / 32};
+    return hga::host_pack_pieces(src, n, dst, wlo, 1, nullptr, no_piece_cb, nullptr) == 1 ? HGA_FLAG_NOT_SIGN : 0;
+}
+
+extern "C" void hga_host_unpack_bits(const uint32_t* src, int64_t n, int8_t* dst) {
+    if (n <= 0) return;
+    const int64_t wlo[2] = {0, (n + 31) / 32};
+    hga::host_unpack_pieces(src, dst, n, wlo, 1, no_piece_cb, nullptr);
+}
