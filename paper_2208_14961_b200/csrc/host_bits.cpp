@@ -14,6 +14,7 @@
 // The device side (bit stream <-> packed column records) is
 // csrc/step_bits.cu.
 #include <immintrin.h>
+#include <pthread.h>
 #include <sched.h>
 
 #include <algorithm>
@@ -22,6 +23,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
+#include <new>
 #include <thread>
 #include <vector>
 
@@ -34,10 +36,10 @@ namespace host {
 class Pool {
    public:
     static Pool& get() {
-        static Pool* p = new Pool();  // never destroyed: workers may outlive static destruction order
+        static Pool* p = make();  // never destroyed: workers may outlive static destruction order
         return *p;
     }
-    int size() const { return (int)workers_.size() + 1; }
+    int size() const { return inline_mode() ? 1 : (int)workers_.size() + 1; }
     // start(): runs fn(ctx, t) for t in [0, ntasks) on the worker threads; the
     // calling thread does not take tasks (it drives the CUDA side meanwhile).
     // wait() returns when all tasks are done.  One job at a time: the job lock
@@ -47,7 +49,7 @@ class Pool {
     void start(int ntasks, void (*fn)(void*, int), void* ctx) {
         job_mu_.lock();
         started_ = ntasks;
-        if (workers_.empty() || ntasks >= (1 << 20)) {
+        if (inline_mode() || ntasks >= (1 << 20)) {
             for (int t = 0; t < ntasks; ++t) fn(ctx, t);  // no workers: run inline (callbacks still see progress)
             started_ = -1;
             return;
@@ -68,9 +70,26 @@ class Pool {
             while (done_.load(std::memory_order_acquire) < started_) _mm_pause();
         job_mu_.unlock();
     }
-    bool inline_mode() const { return workers_.empty(); }
+    // A forked child has none of the parent's worker threads: it runs every
+    // job inline on fresh locks (pthread_atfork below).
+    bool inline_mode() const { return workers_.empty() || forked_; }
 
    private:
+    static Pool* make() {
+        Pool* p = new Pool();
+        instance_ = p;
+        pthread_atfork(nullptr, nullptr, [] {
+            if (Pool* q = instance_) {
+                new (&q->job_mu_) std::mutex();
+                new (&q->mu_) std::mutex();
+                new (&q->cv_) std::condition_variable();
+                q->forked_ = true;
+            }
+        });
+        return p;
+    }
+    static inline Pool* instance_ = nullptr;
+    bool forked_ = false;
     int started_ = 0;
     Pool() {
         int n = 0;

@@ -68,3 +68,25 @@ def test_population_stream_layout():
 def test_empty_and_tiny():
     assert lib.hga_host_pack_bits(None, 0, None) == 0
     lib.hga_host_unpack_bits(None, 0, None)
+
+
+@pytest.mark.filterwarnings("ignore:This process .* is multi-threaded:DeprecationWarning")
+def test_pack_in_a_forked_child():
+    """A child forked after the pool's workers started has none of them: the
+    packer runs inline there instead of waiting for threads that do not exist."""
+    import os
+
+    x = np.random.default_rng(5).choice(np.array([-1, 1], dtype=np.int8), size=300_001)
+    assert _pack(x)[0] == 0  # the parent's pool is running
+    pid = os.fork()
+    if pid == 0:  # child
+        ok = False
+        try:
+            rc, words = _pack(x)
+            back = np.zeros(x.size, dtype=np.int8)
+            lib.hga_host_unpack_bits(words.ctypes.data, x.size, back.ctypes.data)
+            ok = rc == 0 and np.array_equal(words, _pack_np(x)) and np.array_equal(back, x)
+        finally:
+            os._exit(0 if ok else 1)
+    _, status = os.waitpid(pid, 0)
+    assert os.WIFEXITED(status) and os.WEXITSTATUS(status) == 0
