@@ -305,6 +305,13 @@ int hga_step_host(const hga_run_args *args, int8_t *host_pop, int64_t *host_fit,
  * from the stream. */
 int hga_host_pack_bits(const int8_t *src, int64_t n, uint32_t *dst);
 void hga_host_unpack_bits(const uint32_t *src, int64_t n, int8_t *dst);
+/* Bit stream <-> packed column records on the device (orders 4..64,
+ * m % 4 == 0; the stream layout of hga_host_pack_bits): hga_bits_to_cols
+ * also raises HGA_FLAG_NOT_GA in *flag (if not NULL) when a matrix breaks
+ * the GA invariants (column 0 not all +1, an unbalanced column). */
+int hga_bits_to_cols(const uint32_t *bits, int64_t n, int32_t m, uint32_t *cols, int32_t *flag,
+                     void *stream);
+int hga_cols_to_bits(const uint32_t *cols, int64_t n, int32_t m, uint32_t *bits, void *stream);
 size_t hga_step_host_bits_bytes(int64_t n_pairs, int32_t m);
 int hga_step_host_bits(const hga_run_args *args, int8_t *host_pop, int64_t *host_fit, uint32_t *host_bits,
                        uint32_t *dev_bits, const int64_t *state_in, int64_t *state_out, int32_t *flag_out,

@@ -108,6 +108,8 @@ SIGNATURES = {
     "hga_run_prepare": (_int, [ctypes.POINTER(RunArgs), _vp]),
     "hga_run": (_int, [ctypes.POINTER(RunArgs), _vp]),
     "hga_step_host": (_int, [ctypes.POINTER(RunArgs), _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int32, _vp, _vp]),
+    "hga_bits_to_cols": (_int, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp]),
+    "hga_cols_to_bits": (_int, [_vp, ctypes.c_int64, ctypes.c_int32, _vp, _vp]),
     "hga_host_pack_bits": (_int, [_vp, ctypes.c_int64, _vp]),
     "hga_host_unpack_bits": (None, [_vp, ctypes.c_int64, _vp]),
     "hga_step_host_bits_bytes": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int32]),

@@ -90,12 +90,14 @@ __global__ void k_mutate_i8(int8_t* pop, int64_t half, int m, const int64_t* __r
 }
 
 // ----------------------------------------------------------------- select
-// Stable order of the `half` smallest fitness values: histogram over
-// (F - min), exclusive scan, then one warp scatters indices in index order
-// (match_any groups equal values inside a 32-wide chunk, so equal values keep
-// index order -- the stable-argsort tie rule).
-constexpr int64_t kSelMaxRange = 1 << 22;
-constexpr int64_t kSelSmemBins = 40 * 1024;
+// Stable order of the `half` smallest fitness values: the range (min, max)
+// of the values, then a stable LSD radix sort (CUB) of the 22-bit keys
+// F - min with their indices -- equal values keep index order, the
+// stable-argsort tie rule (engine.py:245).  Three digit passes at any
+// population size (round 1 scattered the indices from a histogram with one
+// warp: 0.78 ms at 4N = 40,000).
+constexpr int kSelBits = 22;
+constexpr int64_t kSelMaxRange = (int64_t)1 << kSelBits;
 
 struct SelWs {
     long long mn, mx;
@@ -123,82 +125,34 @@ __global__ void k_sel_init(SelWs* w) {
     w->mx = LLONG_MIN;
 }
 
-__global__ void k_sel_hist(const int64_t* __restrict__ f, int64_t n, const SelWs* w, int32_t* hist,
-                           int32_t* bad_flag) {
+// 22-bit sort keys F - min and their indices; a range of 2^22 or more raises
+// HGA_FLAG_FIT_RANGE (the keys are then clamped and the order is not valid).
+__global__ void k_sel_keys(const int64_t* __restrict__ f, int64_t n, const SelWs* w, uint32_t* __restrict__ keys,
+                           int32_t* __restrict__ idx, int32_t* bad_flag) {
     const long long mn = w->mn;
-    if ((unsigned long long)(w->mx - mn) >= (unsigned long long)kSelMaxRange) {
-        if (blockIdx.x == 0 && threadIdx.x == 0 && bad_flag) atomicOr(bad_flag, HGA_FLAG_FIT_RANGE);
-        return;
+    if ((unsigned long long)(w->mx - mn) >= (unsigned long long)kSelMaxRange && blockIdx.x == 0 && threadIdx.x == 0 &&
+        bad_flag)
+        atomicOr(bad_flag, HGA_FLAG_FIT_RANGE);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long d = (unsigned long long)((long long)f[i] - mn);
+        keys[i] = (uint32_t)min(d, (unsigned long long)(kSelMaxRange - 1));
+        idx[i] = (int32_t)i;
     }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&hist[f[i] - mn], 1);
 }
 
-// Single CTA: scan hist -> start offsets, then the ordered scatter.
-__global__ void __launch_bounds__(1024) k_sel_scatter(const int64_t* __restrict__ f, int64_t n,
-                                                      int64_t half, const SelWs* w, int32_t* hist,
-                                                      int64_t* order) {
-    extern __shared__ int32_t sbins[];
-    __shared__ int32_t warp_tot[32];
-    __shared__ int32_t carry;
-    const long long mn = w->mn;
-    if ((unsigned long long)(w->mx - mn) >= (unsigned long long)kSelMaxRange) return;
-    const int64_t R = w->mx - mn + 1;
-    const bool in_smem = R <= kSelSmemBins;
-    int32_t* cur = in_smem ? sbins : hist;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) carry = 0;
-    __syncthreads();
-    // block-wide exclusive scan over R bins, 1024 at a time
-    for (int64_t b0 = 0; b0 < R; b0 += 1024) {
-        const int64_t b = b0 + tid;
-        const int32_t v = b < R ? hist[b] : 0;
-        int32_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) warp_tot[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            int32_t t = warp_tot[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
-                if (lane >= o) t += y;
-            }
-            warp_tot[lane] = t;
-        }
-        __syncthreads();
-        const int32_t excl = carry + (wid ? warp_tot[wid - 1] : 0) + x - v;
-        if (b < R) cur[b] = excl;
-        __syncthreads();
-        if (tid == 0) carry += warp_tot[31];
-        __syncthreads();
-    }
-    // ordered scatter by warp 0
-    if (wid == 0) {
-        for (int64_t i0 = 0; i0 < n; i0 += 32) {
-            const int64_t i = i0 + lane;
-            int64_t key = -1;
-            int32_t start = 0;
-            if (i < n) {
-                key = f[i] - mn;
-                start = cur[key];
-                if (start >= half) key = -1;
-            }
-            const unsigned peers = __match_any_sync(0xffffffffu, key);
-            if (key >= 0) {
-                const int rank = __popc(peers & ((1u << lane) - 1u));
-                const int64_t pos = (int64_t)start + rank;
-                if (pos < half) order[pos] = i;
-            }
-            __syncwarp();
-            if (key >= 0 && (__ffs(peers) - 1) == lane) cur[key] = start + __popc(peers);
-            __syncwarp();
-        }
-    }
+__global__ void k_sel_order(const int32_t* __restrict__ idx, int64_t k, int64_t* __restrict__ order) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        order[i] = idx[i];
 }
+
+static size_t sel_temp_bytes(int64_t n) {
+    size_t t = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)n, 0, kSelBits);
+    return (t + 255) & ~(size_t)255;
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 // Any-range fallback: stable LSD radix sort of (fitness, index) pairs.  int64
 // keys become order-preserving uint64 (sign bit flipped); CUB's radix sort is
@@ -303,8 +257,9 @@ int hga_mutate_i8(int8_t* pop, int64_t total, int32_t m, const int64_t* cols, co
 int64_t hga_select_max_range(void) { return kSelMaxRange; }
 
 size_t hga_select_ws_bytes(int64_t total) {
-    (void)total;
-    return 256 + (size_t)kSelMaxRange * 4;
+    if (total < 0 || total >= ((int64_t)1 << 31)) return 0;
+    const int64_t n = std::max<int64_t>(total, 1);
+    return 256 + 4 * align256((size_t)n * 4) + sel_temp_bytes(n);
 }
 
 int hga_select_order(const int64_t* fitness, int64_t total, int64_t* order, int32_t* bad_flag, void* ws,
@@ -340,21 +295,26 @@ int hga_select_smallest_radix(const int64_t* fitness, int64_t total, int64_t k, 
 int hga_select_smallest(const int64_t* fitness, int64_t total, int64_t k, int64_t* order, int32_t* bad_flag,
                         void* ws, size_t ws_bytes, void* stream) {
     if (total < 0 || k < 0 || k > total) return HGA_E_INVALID;
-    const int64_t half = k;
-    if (half == 0) return HGA_OK;
+    if (k == 0) return HGA_OK;
+    if (total >= ((int64_t)1 << 31)) return HGA_E_UNSUPPORTED;
     if (!ws || ws_bytes < hga_select_ws_bytes(total)) return HGA_E_WORKSPACE;
     cudaStream_t st = (cudaStream_t)stream;
     SelWs* w = (SelWs*)ws;
-    int32_t* hist = (int32_t*)((char*)ws + 256);
-    cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)kSelMaxRange * 4, st);
-    if (e != cudaSuccess) return to_rc(e);
+    char* p = (char*)ws + 256;
+    const size_t region = align256((size_t)total * 4);
+    uint32_t* keys_in = (uint32_t*)p;
+    uint32_t* keys_out = (uint32_t*)(p + region);
+    int32_t* idx_in = (int32_t*)(p + 2 * region);
+    int32_t* idx_out = (int32_t*)(p + 3 * region);
+    void* temp = p + 4 * region;
+    size_t temp_bytes = sel_temp_bytes(total);
     k_sel_init<<<1, 1, 0, st>>>(w);
     k_sel_minmax<<<grid_1d(total), 256, 0, st>>>(fitness, total, w);
-    k_sel_hist<<<grid_1d(total), 256, 0, st>>>(fitness, total, w, hist, bad_flag);
-    const size_t smem = (size_t)kSelSmemBins * 4;
-    e = cudaFuncSetAttribute(k_sel_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_sel_keys<<<grid_1d(total), 256, 0, st>>>(fitness, total, w, keys_in, idx_in, bad_flag);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, idx_in, idx_out, (int)total, 0,
+                                                    kSelBits, st);
     if (e != cudaSuccess) return to_rc(e);
-    k_sel_scatter<<<1, 1024, smem, st>>>(fitness, total, half, w, hist, order);
+    k_sel_order<<<grid_1d(k), 256, 0, st>>>(idx_out, k, order);
     return to_rc(cudaGetLastError());
 }
 

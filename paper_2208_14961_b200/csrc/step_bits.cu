@@ -182,3 +182,14 @@ int cols_to_bits(const uint32_t* cols, int64_t n, int32_t m, uint32_t* bits, con
 }
 
 }  // namespace hga
+
+extern "C" int hga_bits_to_cols(const uint32_t* bits, int64_t n, int32_t m, uint32_t* cols, int32_t* flag,
+                                void* stream) {
+    if (n < 0 || m < 4 || m > 64 || (m & 3)) return n < 0 ? HGA_E_INVALID : HGA_E_UNSUPPORTED;
+    return hga::bits_to_cols(bits, n, m, cols, flag, (cudaStream_t)stream);
+}
+
+extern "C" int hga_cols_to_bits(const uint32_t* cols, int64_t n, int32_t m, uint32_t* bits, void* stream) {
+    if (n < 0 || m < 4 || m > 64 || (m & 3)) return n < 0 ? HGA_E_INVALID : HGA_E_UNSUPPORTED;
+    return hga::cols_to_bits(cols, n, m, bits, nullptr, (cudaStream_t)stream);
+}

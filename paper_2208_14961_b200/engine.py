@@ -990,8 +990,8 @@ def _step_host(state):
     it0, best0 = int(state.iteration), int(state.best_fitness)
     last0 = int(state.trace[-1]) if state.trace else best0
     explicit = bridge.cfg.rng != "philox"
-    if explicit or res.m > 64 or bridge.bit_buffers() is None:
-        bridge.pin(pop_np)  # DMA copies of the int8 population (the bit-stream path packs it on the host instead)
+    if bridge.bit_buffers() is None:
+        bridge.pin(pop_np)  # DMA copies of the int8 population (the bit-stream paths pack it on the host instead)
     bridge.pin(fit_np)
     if not explicit and res.m <= 64:
         # the whole step is enqueued natively (hga_step_host): chunked copies on a
@@ -1048,10 +1048,20 @@ def _step_host_generic(state, bridge: _HostBridge, pop_np, fit_np, it0: int, bes
     comp, cs = torch.cuda.current_stream(), bridge.copy_stream
     pop_t, fit_t = torch.from_numpy(pop_np), torch.from_numpy(fit_np)
     parts = _chunks(total)
+    bits = bridge.bit_buffers()  # orders 4..64: the population crosses PCIe as a bit stream
+    nb = 4 * ((pop_np.size + 31) // 32)
+    if bits is not None and lib.hga_host_pack_bits(pop_np.ctypes.data, pop_np.size, bits[0].data_ptr()) & FLAG_NOT_SIGN:
+        raise ValueError("step: matrix entries must be +1 or -1")
     cs.wait_stream(comp)
     with torch.cuda.stream(cs):
         res.fit[cur].copy_(fit_t, non_blocking=True)
-    for a, b in parts:
+    if bits is not None:
+        with torch.cuda.stream(cs):
+            bits[1][:nb].copy_(bits[0][:nb], non_blocking=True)
+        comp.wait_stream(cs)
+        check(lib.hga_bits_to_cols(bits[1].data_ptr(), total, m, res.pop[cur].data_ptr(), flag.data_ptr(),
+                                   comp.cuda_stream), "hga_bits_to_cols")
+    for a, b in (parts if bits is None else ()):
         with torch.cuda.stream(cs):
             bridge.pop_i8[a:b].copy_(pop_t[a:b], non_blocking=True)
             landed = torch.cuda.Event()
@@ -1081,7 +1091,10 @@ def _step_host_generic(state, bridge: _HostBridge, pop_np, fit_np, it0: int, bes
         args.flags |= RUN_FORCE  # exactly one generation: the new population is in buffer cur ^ 1
         check(lib.hga_run(args, stream_ptr()), "hga_run")
         new = cur ^ 1
-    for a, b in parts:
+    if bits is not None:
+        check(lib.hga_cols_to_bits(res.pop[new].data_ptr(), total, m, bits[1].data_ptr(), comp.cuda_stream),
+              "hga_cols_to_bits")
+    for a, b in (parts if bits is None else ()):
         check(lib.hga_unpack_i8(res.pop[new][a * mw].data_ptr(), b - a, m, bridge.pop_i8[a].data_ptr(),
                                 comp.cuda_stream), "hga_unpack_i8")
         ready = torch.cuda.Event()
@@ -1091,9 +1104,13 @@ def _step_host_generic(state, bridge: _HostBridge, pop_np, fit_np, it0: int, bes
             pop_t[a:b].copy_(bridge.pop_i8[a:b], non_blocking=True)
     cs.wait_stream(comp)
     with torch.cuda.stream(cs):
+        if bits is not None:
+            bits[0][:nb].copy_(bits[1][:nb], non_blocking=True)
         fit_t.copy_(res.fit[new], non_blocking=True)
         bridge.host_state.copy_(res.dstate, non_blocking=True)
     cs.synchronize()
+    if bits is not None:
+        lib.hga_host_unpack_bits(bits[0].data_ptr(), pop_np.size, pop_np.ctypes.data)
     if explicit:
         it1, fmin = inner.iteration, inner.trace[-1]
     else:
