@@ -283,7 +283,7 @@ def run_ours(args, rank, world, local_rank):
     e2e = run_e2e(args, cfg, hga, engine, torch)
     # the same public call computing exactly what the reference arm computes:
     # reference streams, the reference arm's seed and initial population
-    e2e_same = run_e2e_same_config(args, engine, torch) if not args.no_cpu else None
+    e2e_same = run_e2e_same_config(args, engine, torch) if (not args.no_cpu and world == 1) else None
     # the same public call on the device-resident SearchState (each step reads
     # back its trace entry / best fitness): what run_search-style users get
     st2 = hga.initial_state(cfg)
