@@ -168,6 +168,11 @@ def algorithmic_bytes_per_generation(m: int, n_pairs: int) -> int:
 
 
 def run_ours(args, rank, world, local_rank):
+    if world > 1 and "HGA_HOST_THREADS" not in os.environ:
+        # one host thread pool per rank (the host-state step's bit packing): share the cores
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        local = env_int("LOCAL_WORLD_SIZE", world)
+        os.environ["HGA_HOST_THREADS"] = str(max(1, cores // max(1, local)))
     import torch
 
     torch.cuda.set_device(local_rank)
