@@ -869,6 +869,7 @@ class _HostBridge:
             else:
                 self._bits = (torch.empty(nb, dtype=torch.uint8, pin_memory=True),
                               torch.empty(nb, dtype=torch.uint8, device=self.res.dev))
+                self.bits_ptrs = (self._bits[0].data_ptr(), self._bits[1].data_ptr())
         return self._bits or None
 
     def pin(self, arr: np.ndarray) -> None:
@@ -1000,15 +1001,15 @@ def _step_host(state):
             bridge.args = res.run_args()
             bridge.st_in = (ctypes.c_int64 * 8)()
             bridge.hs_np, bridge.hf_np = bridge.host_state.numpy(), bridge.host_flag.numpy()
+            bridge.ptrs = (bridge.host_state.data_ptr(), bridge.host_flag.data_ptr(), bridge.copy_stream.cuda_stream)
         st_in = bridge.st_in
         st_in[0], st_in[1], st_in[2], st_in[6], st_in[7] = it0, best0, 0, 1, last0
         bits = bridge.bit_buffers()
         if bits is not None:
             # the population crosses PCIe as a bit stream (hga_step_host_bits: 8x fewer bytes)
-            rc = lib.hga_step_host_bits(bridge.args, pop_np.ctypes.data, fit_np.ctypes.data, bits[0].data_ptr(),
-                                        bits[1].data_ptr(), st_in, bridge.host_state.data_ptr(),
-                                        bridge.host_flag.data_ptr(), _BIT_CHUNKS, stream_ptr(),
-                                        bridge.copy_stream.cuda_stream)
+            hs_p, hf_p, cs_p = bridge.ptrs
+            rc = lib.hga_step_host_bits(bridge.args, pop_np.ctypes.data, fit_np.ctypes.data, bridge.bits_ptrs[0],
+                                        bridge.bits_ptrs[1], st_in, hs_p, hf_p, _BIT_CHUNKS, stream_ptr(), cs_p)
         else:
             rc = lib.hga_step_host(bridge.args, pop_np.ctypes.data, fit_np.ctypes.data, bridge.pop_i8.data_ptr(),
                                    st_in, bridge.host_state.data_ptr(), bridge.host_flag.data_ptr(), _HOST_CHUNKS,
