@@ -438,7 +438,11 @@ int hga_fitness_i8(const int8_t* pop, int64_t n, int32_t m, uint32_t variants, i
     cudaStream_t st = (cudaStream_t)stream;
     const int tc_mode = fit_tc_mode();
     const bool al16 = (((uintptr_t)pop) & 15) == 0;
-    if (((tc_mode == 1 && m >= tc2_min_order()) || tc_mode == 4) && al16 && fit_tc2_order(m))
+    // several variants at once (or SQ) at orders 36 / 40: the XOR+POPC kernel's
+    // all-variant build runs at 0.41-0.54e9 evals/s there, the tensor-core kernel
+    // at 1.0e9 (r02_fitness_sweep.csv); F2 or F1 alone stay on XOR+POPC below 44
+    const bool multi = (variants & ~(HGA_VAR_F2 | HGA_VAR_ORTH)) != 0 && variants != HGA_VAR_F1;
+    if (((tc_mode == 1 && (m >= tc2_min_order() || multi)) || tc_mode == 4) && al16 && fit_tc2_order(m))
         return launch_fit_tc2(m, pop, n, variants, f1, f2, orth, sq, bad_flag, st);
     if ((tc_mode == 2 || tc_mode == 3) && al16 && fit_tc_order(m, tc_mode == 2))
         return launch_fit_tc(m, pop, n, variants, f1, f2, orth, sq, bad_flag, st);
