@@ -60,7 +60,7 @@ extern "C" {
 #define HGA_FLAG_NOT_SIGN 1     /* an entry is not +1/-1 */
 #define HGA_FLAG_POINT_RANGE 2  /* crossover point outside [1, m-1] */
 #define HGA_FLAG_PLAN_RANGE 4   /* mutation plan index out of range */
-#define HGA_FLAG_FIT_RANGE 8    /* fitness range exceeds the select histogram */
+#define HGA_FLAG_FIT_RANGE 8    /* fitness range exceeds the select keys (2^22) */
 #define HGA_FLAG_NOT_GA 16      /* hga_pack_i8: column 0 is not all +1 or a column is
                                    unbalanced (the GA invariants, engine.py:440-446) */
 
@@ -149,7 +149,7 @@ int hga_mutate_i8(int8_t *pop, int64_t total, int32_t m, const int64_t *cols,
 int64_t hga_select_max_range(void);
 /* Any-range variant (stable radix sort of all `total` (fitness, index)
  * pairs; any int64 values): the first k indices of the stable argsort.
- * Used when the histogram path raised HGA_FLAG_FIT_RANGE.  total < 2^31. */
+ * Used when hga_select_order raised HGA_FLAG_FIT_RANGE.  total < 2^31. */
 size_t hga_select_radix_ws_bytes(int64_t total);
 int hga_select_smallest_radix(const int64_t *fitness, int64_t total, int64_t k, int64_t *order,
                               void *ws, size_t ws_bytes, void *stream);
