@@ -114,7 +114,10 @@ class Pool {
         }
     }
     void loop() {
-        uint64_t seen = gen_.load(std::memory_order_acquire);
+        // 0, not the current value: a worker that starts running only after the
+        // first job was posted must still see that job (the caller of start() does
+        // not take tasks itself, so a job nobody sees would never finish)
+        uint64_t seen = 0;
         for (;;) {
             // spin a little (back-to-back steps arrive every few hundred us), then sleep
             int spins = 0;

@@ -88,5 +88,16 @@ def test_pack_in_a_forked_child():
             ok = rc == 0 and np.array_equal(words, _pack_np(x)) and np.array_equal(back, x)
         finally:
             os._exit(0 if ok else 1)
-    _, status = os.waitpid(pid, 0)
+    import time
+
+    deadline = time.monotonic() + 60
+    while True:  # never hang the suite on a child that deadlocked
+        done, status = os.waitpid(pid, os.WNOHANG)
+        if done:
+            break
+        if time.monotonic() > deadline:
+            os.kill(pid, 9)
+            os.waitpid(pid, 0)
+            pytest.fail("forked child did not finish")
+        time.sleep(0.01)
     assert os.WIFEXITED(status) and os.WEXITSTATUS(status) == 0
