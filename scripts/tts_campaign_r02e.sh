@@ -5,6 +5,6 @@
 set -u
 out=gpurun_out/${1:-r02tts32}
 mkdir -p $out
-timeout 2700 python scripts/time_to_hadamard.py --order 32 --population 10000 --fitness f2 --nc 1 --nr 12 \
-    --restart-stall 300000 --seeds ${SEEDS32:-0 1 2 3} --budget 600 --out $out/tts32.jsonl > /dev/null 2>> $out/err.log
+timeout 3500 python scripts/time_to_hadamard.py --order 32 --population 10000 --fitness f2 --nc 1 --nr 12 \
+    --restart-stall 300000 --seeds ${SEEDS32:-0 1 2 3} --budget ${BUDGET32:-600} --out $out/tts32.jsonl > /dev/null 2>> $out/err.log
 exit 0
